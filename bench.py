@@ -1,0 +1,389 @@
+"""Benchmark of the B200 stencil hot path (contract: one JSON line on rank 0).
+
+Workload (default): BASELINE.json configs[1] (SURVEY "C2"), the 3D acoustic
+forward at space order 4 on 281^3 (201^3 + 40-point damping layer on every
+face), 10 m spacing, two layers 1.5/2.5 km/s, 10 Hz Ricker source at depth
+20 m, 101 receivers on a line, 1000 ms at dt = 0.4 h / vmax = 1.6 ms
+(625 steps). A benchmark "step" is one full apply of that operator: 625 time
+steps of stencil + injection + sampling, i.e. 277^3 * 625 = 1.328e10
+interior grid-point updates.
+
+  value : GPts/s with every buffer resident in HBM (sf_plan_run, CUDA graph),
+          device-timed with CUDA events, max over ranks.
+  e2e   : GPts/s through the C-ABI entry sf_acoustic_apply with host (pinned)
+          buffers: H2D of all nine arguments, the 625 steps, D2H of the three
+          field slots and both traces, every step.
+  roofline : the stencil kernel's algorithmic bytes (20 B per interior point:
+          read u(t), u(t-1), m, eta, write u(t+1)) / its average launch time.
+
+`--impl reference` times the reference's own CPU implementation (the
+stencilforge library compiled from its sources into oracle/_ref, generated
+C/OpenMP kernel via Operator::apply) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # SURVEY C2 / BASELINE configs[1]
+    "c2": dict(shape=(281, 281, 281), order=4, nt=625, boundary=40, spacing=10.0,
+               v_top=1500.0, v_bottom=2500.0, random=False),
+    # SURVEY C3 / BASELINE configs[2] (one order per run)
+    "c3o4": dict(shape=(512, 512, 512), order=4, nt=500, boundary=40, spacing=10.0,
+                 random=True),
+    "c3o8": dict(shape=(512, 512, 512), order=8, nt=500, boundary=40, spacing=10.0,
+                 random=True),
+    "c3o12": dict(shape=(512, 512, 512), order=12, nt=500, boundary=40, spacing=10.0,
+                  random=True),
+    "c3o16": dict(shape=(512, 512, 512), order=16, nt=500, boundary=40, spacing=10.0,
+                  random=True),
+}
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def smooth_velocity(shape, seed, sigma=8.0, vmin=1500.0, vmax=4500.0):
+    """Seeded N(0,1) noise, separable Gaussian filter (sigma cells, truncate
+    4 sigma, reflect), affinely rescaled to [vmin, vmax]."""
+    from scipy.ndimage import gaussian_filter
+    rng = np.random.default_rng(seed)
+    noise = rng.standard_normal(shape, dtype=np.float32)
+    f = gaussian_filter(noise, sigma=sigma, mode="reflect", truncate=4.0)
+    lo, hi = float(f.min()), float(f.max())
+    return vmin + (vmax - vmin) * (f.astype(np.float64) - lo) / (hi - lo)
+
+
+def make_model(cfg_name):
+    import paper_1609_03361_b200 as sf
+    c = CONFIGS[cfg_name]
+    shape = c["shape"]
+    bw, h = c["boundary"], c["spacing"]
+    if not c["random"]:
+        vmax = max(c["v_top"], c["v_bottom"])
+        model = sf.AcousticModel(shape=shape, boundary_width=bw, spacing=h, nt=c["nt"],
+                                 space_order=c["order"], f0=10.0, v_top=c["v_top"],
+                                 v_bottom=c["v_bottom"])
+        model.dt = 0.4 * h / vmax
+        mid = shape[1] // 2
+        model.src_coords = [[(bw + 2) * h, mid * h, mid * h]]
+        model.rec_coords = [[(bw + 2) * h, mid * h, (bw + 2 * i) * h] for i in range(101)]
+        return model, None, None
+    model = sf.AcousticModel(shape=shape, boundary_width=bw, spacing=h, nt=c["nt"],
+                             space_order=c["order"], f0=10.0, v_top=4500.0, v_bottom=4500.0)
+    model.dt = min(0.4 * h / 4500.0, model.stable_dt())
+    mid = shape[1] // 2
+    model.src_coords = [[(bw + 2) * h, mid * h, mid * h]]
+    lo, hi = (bw + 2) * h, (shape[1] - bw - 3) * h
+    g = np.linspace(lo + 0.37 * h, hi - 0.41 * h, 256)
+    model.rec_coords = [[(bw + 10) * h, y, z] for y in g for z in g]
+    return model, smooth_velocity(shape, 1234), 1500.0
+
+
+def interior_points(model):
+    r = model.space_order // 2
+    n = 1
+    for e in model.shape:
+        n *= e - 2 * r
+    return n
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                smax = float(p[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, p[4:8]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(world, value):
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_reference_sample(model, cfg_name, v_field, v_min, steps=1, warmup=1, budget_s=20.0):
+    """The reference's CPU path (oracle/_ref: stencilforge JIT kernel) on a
+    bounded sample: the full grid for nt_s time steps. Returns GPts/s."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as ol
+    if ol.have_ref():
+        ref = ol.Ref()
+        kind = "reference"
+        threads = ref.max_threads()
+        ref.set_threads(threads)
+        case = ol.AcousticCase(shape=model.shape, nt=1, boundary_width=model.boundary_width,
+                               spacing=model.spacing, dt=model.dt, space_order=model.space_order,
+                               f0=model.f0, v_top=model.v_top, v_bottom=model.v_bottom,
+                               src_coords=model.src_coords, rec_coords=model.rec_coords)
+        # calibrate: time a short run, then size the sample to the budget
+        def timed(nt_s):
+            case.nt = nt_s
+            op = ol.ref_acoustic(ref, case, True)
+            if v_field is not None:
+                port = ol.Port()
+                m, eta = port.medium_from_velocity(v_field, model.boundary_width, model.spacing,
+                                                   v_min)
+                op.set("m", m)
+                op.set("eta", eta)
+            op.build()
+            t0 = time.perf_counter()
+            op.apply()
+            return time.perf_counter() - t0
+        t_cal = timed(4)
+        nt_s = int(max(4, min(model.nt, budget_s / max(t_cal / 4, 1e-6))))
+        for _ in range(warmup):
+            timed(min(nt_s, 4))
+        times = [timed(nt_s) for _ in range(max(1, steps))]
+        secs = float(np.median(times))
+    else:
+        port = ol.Port()
+        kind = "port"
+        import multiprocessing
+        threads = multiprocessing.cpu_count()
+        nt_s = 8
+        m = np.zeros(model.shape, np.float32)
+        eta = np.zeros_like(m)
+        c = port.coefs(3, model.space_order, True, model.dt, model.spacing)
+        u = np.zeros((3,) + tuple(model.shape), np.float32)
+        src_ci, src_w = port.interp(np.array(model.src_coords), model.spacing, model.shape)
+        rec_ci, rec_w = port.interp(np.array(model.rec_coords), model.spacing, model.shape)
+        src = np.ones((nt_s, len(src_ci)), np.float32)
+        rec = np.zeros((nt_s, len(rec_ci)), np.float32)
+        t0 = time.perf_counter()
+        port.acoustic_run(c, u, m + 1.0, eta, src, src_ci, src_w, rec, rec_ci, rec_w, nt_s)
+        secs = time.perf_counter() - t0
+    gpts = interior_points(model) * nt_s / secs / 1e9
+    sample = (f"{cfg_name} grid {'x'.join(map(str, model.shape))} order {model.space_order}, "
+              f"{nt_s} of {model.nt} time steps, median of {max(1, steps)} applies after "
+              f"{warmup} warm-up, JIT excluded")
+    return {"value": gpts, "unit": "GPts/s", "cores": threads, "kind": kind, "sample": sample}
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    model, v, vmin = make_model(args.config)
+    base = cpu_reference_sample(model, args.config, v, vmin, steps=args.steps,
+                                warmup=args.warmup, budget_s=args.cpu_budget)
+    line = {
+        "impl": "reference", "metric": "GPts/s (grid-point updates/sec)", "value": base["value"],
+        "unit": "GPts/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": config_block(args, model),
+        "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": "GPts/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, model):
+    c = CONFIGS[args.config]
+    return {"workload": f"{args.config}: 3D acoustic forward, space order {model.space_order}, "
+                        f"{'x'.join(map(str, model.shape))} (boundary {c['boundary']}), "
+                        f"{model.nt} time steps, dt {model.dt:.6g} s, "
+                        f"{len(model.rec_coords)} receivers",
+            "grid": list(model.shape), "space_order": model.space_order, "nt": model.nt,
+            "interior_points": interior_points(model), "parallelism": f"replicas{args.gpus}",
+            "l2": "working set (3 u slots + m + eta) larger than the 126 MB L2; no flush needed"}
+
+
+def run_b200_arm(args, world, rank, local):
+    import paper_1609_03361_b200 as sf
+    model, v, vmin = make_model(args.config)
+    setup = sf.acoustic_build(model, True, device=local, v_field=v, v_min=vmin, pinned=True)
+    op = setup.op
+    pts = interior_points(model)
+    r = model.space_order // 2
+    # resident: upload once, warm up (graph capture + clocks), then time
+    op.upload()
+    for _ in range(args.warmup):
+        op.run(0, model.nt)
+    op.synchronize()
+    tot_ms, sten_ms, launches_per_run = op.time(stencil=True)
+    import torch
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    barrier(world)
+    with ClockSampler(local) as clocks:
+        evs = []
+        torch.cuda.synchronize()
+        barrier(world)
+        t_wall = time.perf_counter()
+        total = 0.0
+        for _ in range(args.steps):
+            t, _, _ = op.time(stencil=False)
+            total += t
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    barrier(world)
+    ms_per_step = max_over_ranks(world, total / args.steps)
+    value = world * pts * model.nt / (ms_per_step / 1e3) / 1e9
+    # stencil-only pass: average launch duration of the dominant kernel
+    stencil_launch_ms = sten_ms / model.nt
+    alg_bytes = 20 * pts
+    peak, peak_kind = load_peaks()
+    achieved = alg_bytes / (stencil_launch_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config)
+        except Exception:
+            traffic = None
+    # e2e through the C-ABI apply with pinned host buffers
+    h2d = sum(a.data.nbytes for a in op.args)
+    d2h = setup.field.data.nbytes + setup.src.data.data.nbytes + setup.rec.data.data.nbytes
+    op.apply()  # warm
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        op.apply()
+    e2e_s = max_over_ranks(world, (time.perf_counter() - t0) / args.steps)
+    e2e = world * pts * model.nt / e2e_s / 1e9
+    if rank != 0:
+        return
+    base = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            base = cpu_reference_sample(model, args.config, v, vmin, steps=1, warmup=1,
+                                        budget_s=args.cpu_budget)
+        except Exception as e:  # reported, not fatal
+            base = {"error": str(e)}
+    line = {
+        "metric": "GPts/s (grid-point updates/sec)", "value": value, "unit": "GPts/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_block(args, model),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": peak_kind,
+                     "kernel": f"acoustic3d_kernel<R={r}> avg launch {stencil_launch_ms * 1e3:.1f} us",
+                     "alg_bytes_per_launch": alg_bytes},
+        "stencil_share": sten_ms / tot_ms if tot_ms > 0 else None,
+        "cpu_baseline": base,
+        "e2e": {"value": e2e, "unit": "GPts/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches_per_run * args.steps),
+        "clocks": clocks.summary(),
+        "wall_s_timed_region": t_wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_init(args)
+    try:
+        if args.impl == "reference":
+            run_reference_arm(args, world, rank)
+        else:
+            run_b200_arm(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,169 @@
+/* include/sf_b200.h — C ABI of the B200-native stencil hot path.
+ *
+ * Drop-in boundary for the reference's generated-kernel FFI. In the reference
+ * (stencilforge, /root/reference/proj) Operator::build() JIT-compiles C99 and
+ * dlsym()s an entry with the signature
+ *
+ *     int Operator(float *u_vec, float *m_vec, float *eta_vec, float *src_vec,
+ *                  int *src_ci_vec, float *src_w_vec, float *rec_vec,
+ *                  int *rec_ci_vec, float *rec_w_vec);      (golden acoustic_3d.c:3)
+ *     int Operator(float *u_vec);                          (golden diffusion_1000.c:3)
+ *
+ * which Operator::apply() calls through CompiledKernel::invoke(span<void*>)
+ * (jit.cpp:104-148, op.cpp:126-161): one flat dense pointer per referenced
+ * GridFunction in grid declaration order (codegen.cpp:398-409), shapes and
+ * folded constants baked in at build time, all nt steps run in one call,
+ * status 0 on success (codegen.cpp:499). This header replaces that pair:
+ *
+ *   jit_compile(source, cfg, sig)      jit.cpp:150-195  -> sf_*_plan_create
+ *   CompiledKernel::invoke(args)       jit.cpp:104-148  -> sf_plan_invoke
+ *   generated Operator(u, m, eta, ...) acoustic_3d.c:3  -> sf_acoustic_apply
+ *   generated Operator(u)              diffusion_1000.c -> sf_diffusion_apply
+ *
+ * Buffers passed to apply/invoke are HOST pointers in the reference's dense
+ * row-major layout with the time slot slowest (grid.cpp:89-101). The plan keeps
+ * HBM-resident padded mirrors; the call uploads, runs every step on the GPU,
+ * and downloads every written buffer (all time slots, sparse series), which is
+ * what the reference leaves in host memory on return.
+ *
+ * Errors: every entry returns an sf_status; sf_last_error() gives the message
+ * (thread-local). There is no CPU fallback: without a usable sm_100 device the
+ * plan constructors fail with SF_ERR_CUDA.
+ */
+#ifndef SF_B200_H
+#define SF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SF_OK = 0,
+    SF_ERR_INVALID = 1,        /* bad argument (InvalidShape/InvalidOrder, error.hpp) */
+    SF_ERR_CFL = 2,            /* CflViolationError (acoustic.cpp:133-137) */
+    SF_ERR_OUT_OF_DOMAIN = 3,  /* OutOfDomainError (sparse.cpp:19-25) */
+    SF_ERR_SIGNATURE = 4,      /* SignatureMismatchError (op.cpp:135-155) */
+    SF_ERR_KERNEL = 5,         /* KernelFailedError (op.cpp:156-159) */
+    SF_ERR_CUDA = 6,           /* device missing / CUDA runtime failure */
+    SF_ERR_OOM = 7             /* device allocation failed */
+} sf_status;
+
+typedef struct sf_plan sf_plan;
+
+/* What the reference bakes into the generated acoustic kernel at build time
+ * (acoustic.cpp:128-200 -> op.cpp:55-92 -> codegen.cpp:411-502). */
+typedef struct {
+    int ndim;            /* 2 or 3 spatial dimensions */
+    int64_t shape[3];    /* spatial extents, axis 0 slowest (boundary included) */
+    int space_order;     /* even, 2..16 */
+    int forward;         /* 1: forward u (t = 0..nt-1); 0: adjoint v (t = nt..1) */
+    int64_t nt;          /* time steps */
+    double dt;           /* seconds (effective dt; CFL checked by the caller) */
+    double spacing;      /* metres, equal on every axis */
+    int64_t n_src;       /* points in the "src" set */
+    int64_t n_rec;       /* points in the "rec" set */
+} sf_acoustic_desc;
+
+/* DiffusionConfig (diffusion.hpp:13-26) with exact rational alpha and dx=dy. */
+typedef struct {
+    int64_t nx, ny;
+    int order;           /* even, 2..16 */
+    int64_t nt;
+    int64_t alpha_num, alpha_den;
+    int64_t dx_num, dx_den;
+} sf_diffusion_desc;
+
+const char *sf_last_error(void);
+int sf_device_count(void);
+
+/* ---- plans (== jit_compile) ------------------------------------------- */
+int sf_acoustic_plan_create(const sf_acoustic_desc *desc, int device, sf_plan **out);
+int sf_diffusion_plan_create(const sf_diffusion_desc *desc, int device, sf_plan **out);
+void sf_plan_destroy(sf_plan *plan);
+
+/* Number of buffers the entry takes and their names in declaration order
+ * (KernelSignature, codegen.hpp:21-29). */
+int sf_plan_num_args(const sf_plan *plan);
+const char *sf_plan_arg_name(const sf_plan *plan, int i);
+/* Byte size of argument i in the dense reference layout. */
+int64_t sf_plan_arg_bytes(const sf_plan *plan, int i);
+
+/* ---- the generated-kernel entries (== Operator(...)) --------------------
+ * Acoustic, forward run: (u, m, eta, src, src_ci, src_w, rec, rec_ci, rec_w)
+ * Acoustic, adjoint run: (v, m, eta, src, src_ci, src_w, rec, rec_ci, rec_w)
+ *   forward injects src[t] into level t+1 and samples rec[t];
+ *   adjoint injects rec[t-1] into level t-1 and samples src[t-1].          */
+int sf_acoustic_apply(sf_plan *plan, float *u_vec, float *m_vec, float *eta_vec,
+                      float *src_vec, int *src_ci_vec, float *src_w_vec,
+                      float *rec_vec, int *rec_ci_vec, float *rec_w_vec);
+int sf_diffusion_apply(sf_plan *plan, float *u_vec);
+/* CompiledKernel::invoke: args in signature order, nargs checked. */
+int sf_plan_invoke(sf_plan *plan, void *const *args, int nargs);
+
+/* ---- HBM-resident control (benchmarks, FWI, multi-step drivers) ---------
+ * upload: host args -> device mirrors (NULL entries skipped);
+ * run:    steps [step_begin, step_end) of the time loop on the device
+ *         (step index k = 0..nt-1 maps to reference t = k forward,
+ *          t = nt-k adjoint), no host copies;
+ * download: device mirrors -> host args (NULL entries skipped).          */
+int sf_plan_upload(sf_plan *plan, void *const *args, int nargs);
+int sf_plan_run(sf_plan *plan, int64_t step_begin, int64_t step_end);
+int sf_plan_download(sf_plan *plan, void *const *args, int nargs);
+int sf_plan_synchronize(sf_plan *plan);
+
+/* Device-timed run of all nt steps from the current resident state, CUDA
+ * events on the plan's stream. total_ms: whole loop; stencil_ms: summed time
+ * of the stencil launches measured in a separate identical pass (NULL to
+ * skip). Restores nothing: callers re-upload between timed runs. */
+int sf_plan_time(sf_plan *plan, float *total_ms, float *stencil_ms,
+                 int64_t *kernel_launches);
+
+/* ---- FWI gradient (config 5; no reference implementation) -------------
+ * Forward with full history in HBM (nt+2 levels), then the adjoint sweep
+ * fused with grad += u(t) * vtt(t) on the interior.
+ * forward plan: fwd desc; args (m, eta, src, src_ci, src_w, rec_ci, rec_w)
+ * residual: rec-shaped [nt][n_rec] series injected by the adjoint.
+ * Outputs: rec traces of the forward [nt][n_rec], gradient (dense field).  */
+int sf_fwi_plan_create(const sf_acoustic_desc *desc, int device, sf_plan **out);
+int sf_fwi_gradient(sf_plan *plan, const float *m, const float *eta,
+                    const float *src, const int *src_ci, const float *src_w,
+                    const int *rec_ci, const float *rec_w, const float *residual,
+                    float *rec_out, float *grad_out, float *v_out /* 3 slots or NULL */,
+                    float *src_adj_out /* [nt][n_src] or NULL */);
+int sf_fwi_time(sf_plan *plan, float *fwd_ms, float *adj_ms);
+
+/* ---- host-side setup mirrors of the reference (no GPU needed) --------- */
+/* interpolation_weights (sparse.cpp:11-41), weights narrowed to f32 as
+ * GridFunction::set stores them. Returns SF_ERR_OUT_OF_DOMAIN outside. */
+int sf_interpolation_weights(int ndim, const double *coord, double spacing,
+                             const int64_t *extents, int32_t *cell, float *w);
+/* AcousticModel::stable_dt (acoustic.cpp:20-34) */
+double sf_stable_dt(int ndim, int space_order, double spacing, double v_top,
+                    double v_bottom);
+/* ricker_wavelet (acoustic.cpp:10-14) */
+double sf_ricker(double f0, double t, double t0);
+/* build_medium (acoustic.cpp:67-105); v_field != NULL overrides the
+ * two-layer velocity with a per-cell field (random media), v_min sets the
+ * sponge strength. */
+int sf_build_medium(int ndim, const int64_t *shape, int boundary_width,
+                    double spacing, double v_top, double v_bottom,
+                    const double *v_field, double v_min, float *m, float *eta);
+/* Folded fp32 stencil constants the plan uses (for inspection/tests):
+ * out[0]=ce, [1]=cm, [2..4]=time-term coefficients in emitted order,
+ * [5]=centre, [6..6+r)=neighbour j=1..r, [14]=injection scale;
+ * time_sel[k] = 2*field(0 eta,1 m) + level(0 prev,1 cur). */
+int sf_acoustic_constants(int ndim, int space_order, int forward, double dt,
+                          double spacing, float *out /* [15] */, int *time_sel /* [3] */);
+
+/* Folded diffusion constants (exact rationals -> double -> f32). */
+int sf_diffusion_constants(int order, int64_t alpha_num, int64_t alpha_den, int64_t dx_num,
+                           int64_t dx_den, float *c0, int *has_c0, float *cj /* [8] */);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -13,6 +13,8 @@
 // row-major layout (slot slowest, grid.cpp:89-101).
 #include <omp.h>
 
+#include <random>
+
 #include <cstring>
 #include <memory>
 #include <string>
@@ -219,3 +221,32 @@ int sfref_interp_weights(int ndim, const double* coord, double spacing,
 }
 
 } // extern "C"
+
+extern "C" {
+// std::mt19937_64(seed) + std::uniform_real_distribution<double>(lo, hi),
+// the draw sequence adjoint_test uses (acoustic.cpp:230-235).
+void sfref_mt_uniform(unsigned seed, long n, double lo, double hi, double* out) {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> dist(lo, hi);
+    for (long i = 0; i < n; ++i) out[i] = dist(rng);
+}
+
+// adjoint_test (acoustic.cpp:223-237) through the reference: fills the
+// four products, returns 0.
+int sfref_adjoint_test(int ndim, const long* shape, int boundary_width, double spacing,
+                       long nt, int order, unsigned seed, double* out4) {
+    return guard([&] {
+        AcousticModel m;
+        m.shape.assign(shape, shape + ndim);
+        m.boundary_width = boundary_width;
+        m.spacing = spacing;
+        m.nt = nt;
+        m.space_order = order;
+        AdjointTestResult r = adjoint_test(m, seed);
+        out4[0] = r.forward_product;
+        out4[1] = r.adjoint_product;
+        out4[2] = r.difference;
+        out4[3] = r.ratio;
+    });
+}
+}

@@ -1,0 +1,978 @@
+// plan.cu — HBM-resident plans, the CUDA-graph time loop and the C ABI
+// (include/sf_b200.h) that replaces the reference's JIT'd Operator() entry.
+//
+// Reference call path being replaced:
+//   Operator::apply (op.cpp:126-161) -> CompiledKernel::invoke (jit.cpp:104-148)
+//   -> generated Operator(u, m, eta, src, src_ci, src_w, rec, rec_ci, rec_w):
+//        for t: aliases (K6) -> stencil (K2/K3) -> inject (K4) -> sample (K5)
+// Here: plan create = build time (constants folded, buffers allocated in HBM),
+// apply = H2D, nt steps replayed from a cached CUDA graph, D2H.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/sf_b200.h"
+#include "kernels.cuh"
+#include "sf_internal.h"
+
+namespace sfb {
+
+namespace {
+thread_local std::string g_error;
+
+struct Status : std::runtime_error {
+    int code;
+    Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define SF_CUDA(expr)                                                                    \
+    do {                                                                                 \
+        cudaError_t e_ = (expr);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            throw Status(e_ == cudaErrorMemoryAllocation ? SF_ERR_OOM : SF_ERR_CUDA,     \
+                         std::string(#expr) + ": " + cudaGetErrorString(e_));            \
+    } while (0)
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+template <typename T>
+T* dalloc(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    SF_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+void dfree(void* p) {
+    if (p) cudaFree(p);
+}
+
+} // namespace
+
+void set_error(const std::string& msg) { g_error = msg; }
+
+// One sparse point set ("src" or "rec") on the device, plus the injection CSR
+// when the set injects.
+struct PointSet {
+    int64_t np = 0;
+    int64_t nt = 0;
+    float* series = nullptr;  // [nt][np]
+    int* ci = nullptr;        // [np][ndim]
+    float* w = nullptr;       // [np][2^ndim]
+    // injection CSR over distinct target cells
+    int ncells = 0;
+    int64_t* cell_off = nullptr;
+    int* start = nullptr;
+    int* cp = nullptr;
+    float* cw = nullptr;
+    std::vector<int32_t> host_ci;  // last uploaded indices (validated)
+};
+
+} // namespace sfb
+
+struct sf_plan {
+    enum Kind { ACOUSTIC, DIFFUSION, FWI } kind;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int ndim = 3;
+    int64_t n[3] = {1, 1, 1};
+    int64_t pitch = 0, plane = 0, slot_elems = 0;
+    int64_t nt = 0;
+    int nslots = 3;
+    sfb::AcousticConstants ac{};       // constants the launchers use
+    sfb::AcousticConstants ac_fwd{}, ac_adj{};  // FWI: both directions
+    sfb::DiffusionConstants dc{};
+    // device mirrors
+    float* slot[3] = {nullptr, nullptr, nullptr};
+    float* m = nullptr;
+    float* eta = nullptr;
+    sfb::PointSet src, rec;
+    // FWI
+    float* hist = nullptr;  // (nt+2) levels
+    float* grad = nullptr;
+    float* v[3] = {nullptr, nullptr, nullptr};
+    // launch geometry
+    dim3 grid3, block3;
+    int zchunk = 0;
+    std::map<std::pair<int64_t, int64_t>, cudaGraphExec_t> graphs;
+    std::vector<std::string> arg_names;
+    std::vector<int64_t> arg_bytes;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int64_t launches_per_step = 0;
+
+    ~sf_plan();
+};
+
+namespace sfb {
+namespace {
+
+using Plan = sf_plan;
+
+int64_t field_numel(const Plan& p) {
+    int64_t v = 1;
+    for (int i = 0; i < p.ndim; ++i) v *= p.n[i];
+    return v;
+}
+
+// rows of the dense reference layout (product of all but the last axis)
+int64_t dense_rows(const Plan& p) { return field_numel(p) / p.n[p.ndim - 1]; }
+
+void h2d_field(const Plan& p, float* dst, const float* src) {
+    const int64_t last = p.n[p.ndim - 1];
+    SF_CUDA(cudaMemcpy2DAsync(dst, p.pitch * sizeof(float), src, last * sizeof(float),
+                              last * sizeof(float), dense_rows(p), cudaMemcpyHostToDevice,
+                              p.stream));
+}
+
+void d2h_field(const Plan& p, float* dst, const float* src) {
+    const int64_t last = p.n[p.ndim - 1];
+    SF_CUDA(cudaMemcpy2DAsync(dst, last * sizeof(float), src, p.pitch * sizeof(float),
+                              last * sizeof(float), dense_rows(p), cudaMemcpyDeviceToHost,
+                              p.stream));
+}
+
+int64_t device_offset(const Plan& p, const int32_t* c) {
+    if (p.ndim == 3) return c[0] * p.plane + static_cast<int64_t>(c[1]) * p.pitch + c[2];
+    return c[0] * p.pitch + c[1];
+}
+
+void alloc_points(Plan& p, PointSet& s, int64_t np, int64_t nt) {
+    s.np = np;
+    s.nt = nt;
+    const int corners = 1 << p.ndim;
+    s.series = dalloc<float>(static_cast<size_t>(std::max<int64_t>(nt, 1) * np));
+    s.ci = dalloc<int>(static_cast<size_t>(np * p.ndim));
+    s.w = dalloc<float>(static_cast<size_t>(np * corners));
+    SF_CUDA(cudaMemsetAsync(s.series, 0, sizeof(float) * std::max<int64_t>(nt, 1) * np, p.stream));
+    SF_CUDA(cudaMemsetAsync(s.ci, 0, sizeof(int) * np * p.ndim, p.stream));
+    SF_CUDA(cudaMemsetAsync(s.w, 0, sizeof(float) * np * corners, p.stream));
+    s.host_ci.assign(static_cast<size_t>(np * p.ndim), 0);
+}
+
+void free_points(PointSet& s) {
+    dfree(s.series);
+    dfree(s.ci);
+    dfree(s.w);
+    dfree(s.cell_off);
+    dfree(s.start);
+    dfree(s.cp);
+    dfree(s.cw);
+    s = PointSet{};
+}
+
+// Validate indices (the reference would index out of bounds silently) and
+// build the deterministic injection CSR: distinct target cells, each with its
+// (p, w[p][k]) contributions in ascending p.
+void upload_points(Plan& p, PointSet& s, const float* series, const int* ci, const float* w,
+                   bool injects) {
+    const int corners = 1 << p.ndim;
+    if (series)
+        SF_CUDA(cudaMemcpyAsync(s.series, series, sizeof(float) * s.nt * s.np,
+                                cudaMemcpyHostToDevice, p.stream));
+    if (ci) {
+        for (int64_t q = 0; q < s.np; ++q)
+            for (int d = 0; d < p.ndim; ++d) {
+                const int v = ci[q * p.ndim + d];
+                if (v < 0 || v > p.n[d] - 2)
+                    throw Status(SF_ERR_INVALID, "sparse cell index out of range at point " +
+                                                     std::to_string(q));
+            }
+        s.host_ci.assign(ci, ci + s.np * p.ndim);
+        SF_CUDA(cudaMemcpyAsync(s.ci, ci, sizeof(int) * s.np * p.ndim, cudaMemcpyHostToDevice,
+                                p.stream));
+    }
+    if (w)
+        SF_CUDA(cudaMemcpyAsync(s.w, w, sizeof(float) * s.np * corners, cudaMemcpyHostToDevice,
+                                p.stream));
+    if (!injects || !(ci || w)) return;
+    if (!w || !ci)
+        throw Status(SF_ERR_INVALID, "injection needs cell indices and weights together");
+    struct Contrib {
+        int64_t off;
+        int p;
+        float w;
+    };
+    std::vector<Contrib> cs;
+    cs.reserve(static_cast<size_t>(s.np * corners));
+    for (int64_t q = 0; q < s.np; ++q)
+        for (int k = 0; k < corners; ++k) {
+            int32_t c[3];
+            for (int d = 0; d < p.ndim; ++d) c[d] = s.host_ci[q * p.ndim + d] + ((k >> d) & 1);
+            cs.push_back({device_offset(p, c), static_cast<int>(q), w[q * corners + k]});
+        }
+    // stable sort by cell keeps ascending p within a cell
+    std::stable_sort(cs.begin(), cs.end(),
+                     [](const Contrib& a, const Contrib& b) { return a.off < b.off; });
+    std::vector<int64_t> cells;
+    std::vector<int> start, cp;
+    std::vector<float> cw;
+    for (size_t i = 0; i < cs.size(); ++i) {
+        if (i == 0 || cs[i].off != cs[i - 1].off) {
+            cells.push_back(cs[i].off);
+            start.push_back(static_cast<int>(i));
+        }
+        cp.push_back(cs[i].p);
+        cw.push_back(cs[i].w);
+    }
+    start.push_back(static_cast<int>(cs.size()));
+    dfree(s.cell_off);
+    dfree(s.start);
+    dfree(s.cp);
+    dfree(s.cw);
+    s.ncells = static_cast<int>(cells.size());
+    s.cell_off = dalloc<int64_t>(cells.size());
+    s.start = dalloc<int>(start.size());
+    s.cp = dalloc<int>(cp.size());
+    s.cw = dalloc<float>(cw.size());
+    // synchronous copies: the host vectors die at scope exit
+    SF_CUDA(cudaStreamSynchronize(p.stream));
+    SF_CUDA(cudaMemcpy(s.cell_off, cells.data(), cells.size() * sizeof(int64_t),
+                       cudaMemcpyHostToDevice));
+    SF_CUDA(cudaMemcpy(s.start, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice));
+    SF_CUDA(cudaMemcpy(s.cp, cp.data(), cp.size() * sizeof(int), cudaMemcpyHostToDevice));
+    SF_CUDA(cudaMemcpy(s.cw, cw.data(), cw.size() * sizeof(float), cudaMemcpyHostToDevice));
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers
+
+template <bool FWD, bool GRAD>
+void launch_acoustic3d_r(int r, dim3 g, dim3 b, cudaStream_t st, const StencilArgs& A) {
+    switch (r) {
+#define SF_CASE(RR)                                                                 \
+    case RR:                                                                        \
+        acoustic3d_kernel<RR, FWD, 16, GRAD><<<g, b, 0, st>>>(A);                   \
+        break;
+        SF_CASE(1) SF_CASE(2) SF_CASE(3) SF_CASE(4) SF_CASE(5) SF_CASE(6) SF_CASE(7) SF_CASE(8)
+#undef SF_CASE
+        default:
+            throw Status(SF_ERR_INVALID, "radius out of range");
+    }
+}
+
+template <bool FWD>
+void launch_acoustic2d_r(int r, dim3 g, dim3 b, cudaStream_t st, const StencilArgs& A) {
+    switch (r) {
+#define SF_CASE(RR)                                              \
+    case RR:                                                     \
+        acoustic2d_kernel<RR, FWD><<<g, b, 0, st>>>(A);          \
+        break;
+        SF_CASE(1) SF_CASE(2) SF_CASE(3) SF_CASE(4) SF_CASE(5) SF_CASE(6) SF_CASE(7) SF_CASE(8)
+#undef SF_CASE
+        default:
+            throw Status(SF_ERR_INVALID, "radius out of range");
+    }
+}
+
+void launch_diffusion_r(int r, dim3 g, dim3 b, cudaStream_t st, const DiffusionArgs& A) {
+    switch (r) {
+#define SF_CASE(RR)                                              \
+    case RR:                                                     \
+        diffusion_kernel<RR><<<g, b, 0, st>>>(A);                \
+        break;
+        SF_CASE(1) SF_CASE(2) SF_CASE(3) SF_CASE(4) SF_CASE(5) SF_CASE(6) SF_CASE(7) SF_CASE(8)
+#undef SF_CASE
+        default:
+            throw Status(SF_ERR_INVALID, "radius out of range");
+    }
+}
+
+StencilArgs stencil_args(const Plan& p, float* out, const float* cur, const float* prev) {
+    StencilArgs A{};
+    A.out = out;
+    A.cur = cur;
+    A.prev = prev;
+    A.m = p.m;
+    A.eta = p.eta;
+    A.pitch = p.pitch;
+    A.plane = p.plane;
+    A.n0 = static_cast<int>(p.n[0]);
+    A.n1 = static_cast<int>(p.n[1]);
+    A.n2 = static_cast<int>(p.ndim == 3 ? p.n[2] : 1);
+    A.zchunk = p.zchunk;
+    A.ce = p.ac.ce;
+    A.cm = p.ac.cm;
+    for (int k = 0; k < 3; ++k) A.tc[k] = p.ac.tc[k];
+    A.c0 = p.ac.c0;
+    for (int j = 0; j < 8; ++j) A.cj[j] = p.ac.cj[j];
+    return A;
+}
+
+void launch_stencil(const Plan& p, float* out, const float* cur, const float* prev,
+                    float* grad = nullptr, const float* uhist = nullptr) {
+    StencilArgs A = stencil_args(p, out, cur, prev);
+    A.grad = grad;
+    A.uhist = uhist;
+    const int r = p.ac.radius;
+    if (p.ndim == 3) {
+        if (grad) {
+            launch_acoustic3d_r<false, true>(r, p.grid3, p.block3, p.stream, A);
+        } else if (p.ac.forward) {
+            launch_acoustic3d_r<true, false>(r, p.grid3, p.block3, p.stream, A);
+        } else {
+            launch_acoustic3d_r<false, false>(r, p.grid3, p.block3, p.stream, A);
+        }
+    } else {
+        dim3 b(64, 4);
+        dim3 g(static_cast<unsigned>((p.n[1] + 63) / 64), static_cast<unsigned>((p.n[0] + 3) / 4));
+        if (p.ac.forward)
+            launch_acoustic2d_r<true>(r, g, b, p.stream, A);
+        else
+            launch_acoustic2d_r<false>(r, g, b, p.stream, A);
+    }
+}
+
+void launch_inject(const Plan& p, const PointSet& s, float* field, int64_t row) {
+    if (s.ncells == 0 || s.np == 0) return;
+    InjectArgs A{};
+    A.field = field;
+    A.m = p.m;
+    A.row = s.series + row * s.np;
+    A.cell_off = s.cell_off;
+    A.start = s.start;
+    A.cp = s.cp;
+    A.cw = s.cw;
+    A.scale = p.ac.src_scale;
+    A.ncells = s.ncells;
+    inject_kernel<<<(s.ncells + 255) / 256, 256, 0, p.stream>>>(A);
+}
+
+void launch_sample(const Plan& p, const PointSet& s, const float* field, int64_t row) {
+    if (s.np == 0) return;
+    SampleArgs A{};
+    A.field = field;
+    A.ci = s.ci;
+    A.w = s.w;
+    A.out = s.series + row * s.np;
+    A.pitch = p.pitch;
+    A.plane = p.plane;
+    A.np = static_cast<int>(s.np);
+    const unsigned g = static_cast<unsigned>((s.np + 255) / 256);
+    if (p.ndim == 3)
+        sample_kernel<3><<<g, 256, 0, p.stream>>>(A);
+    else
+        sample_kernel<2><<<g, 256, 0, p.stream>>>(A);
+}
+
+// One step of the reference time loop. Step k maps to t = k (forward) or
+// t = nt - k (adjoint); slot aliases as in codegen.cpp:336-354.
+void enqueue_acoustic_step(Plan& p, int64_t k, float* const* u, bool stencil_only = false) {
+    if (p.ac.forward) {
+        const int64_t t = k;
+        float* prev = u[(t + 2) % 3];
+        float* cur = u[t % 3];
+        float* out = u[(t + 1) % 3];
+        launch_stencil(p, out, cur, prev);
+        if (stencil_only) return;
+        launch_inject(p, p.src, out, t);
+        launch_sample(p, p.rec, out, t);
+    } else {
+        const int64_t t = p.nt - k;
+        float* out = u[(t + 2) % 3];
+        float* cur = u[t % 3];
+        float* prev = u[(t + 1) % 3];
+        launch_stencil(p, out, cur, prev);
+        if (stencil_only) return;
+        launch_inject(p, p.rec, out, t - 1);
+        launch_sample(p, p.src, out, t - 1);
+    }
+}
+
+void enqueue_diffusion_step(Plan& p, int64_t t) {
+    DiffusionArgs A{};
+    A.cur = p.slot[t % 2];
+    A.out = p.slot[(t + 1) % 2];
+    A.pitch = p.pitch;
+    A.n0 = static_cast<int>(p.n[0]);
+    A.n1 = static_cast<int>(p.n[1]);
+    A.c0 = p.dc.c0;
+    A.has_c0 = p.dc.has_c0;
+    for (int j = 0; j < 8; ++j) A.cj[j] = p.dc.cj[j];
+    dim3 b(64, 4);
+    dim3 g(static_cast<unsigned>((p.n[1] + 63) / 64), static_cast<unsigned>((p.n[0] + 3) / 4));
+    launch_diffusion_r(p.dc.radius, g, b, p.stream, A);
+}
+
+// FWI phases (config 5): forward into the HBM history, then the adjoint
+// sweep with the delayed gradient term fused into the stencil.
+void enqueue_fwi_forward(Plan& p) {
+    p.ac = p.ac_fwd;
+    const int64_t L = p.slot_elems;
+    SF_CUDA(cudaMemsetAsync(p.hist, 0, sizeof(float) * 2 * L, p.stream));
+    for (int64_t t = 0; t < p.nt; ++t) {
+        float* out = p.hist + (t + 2) * L;
+        launch_stencil(p, out, p.hist + (t + 1) * L, p.hist + t * L);
+        launch_inject(p, p.src, out, t);
+        launch_sample(p, p.rec, out, t);
+    }
+}
+
+void enqueue_fwi_adjoint(Plan& p) {
+    p.ac = p.ac_adj;  // adjoint term order and direction (acoustic.cpp:187-198)
+    const int64_t L = p.slot_elems;
+    for (int s = 0; s < 3; ++s) SF_CUDA(cudaMemsetAsync(p.v[s], 0, sizeof(float) * L, p.stream));
+    SF_CUDA(cudaMemsetAsync(p.grad, 0, sizeof(float) * L, p.stream));
+    for (int64_t t = p.nt; t >= 1; --t) {
+        float* out = p.v[(t + 2) % 3];
+        const float* cur = p.v[t % 3];
+        const float* prev = p.v[(t + 1) % 3];
+        if (t <= p.nt - 1)  // term for time t+1: v(t+2) is still in `out`
+            launch_stencil(p, out, cur, prev, p.grad, p.hist + (t + 2) * L);
+        else
+            launch_stencil(p, out, cur, prev);
+        launch_inject(p, p.rec, out, t - 1);
+        launch_sample(p, p.src, out, t - 1);
+    }
+    if (p.nt >= 1) {  // term for time 1
+        dim3 b(128);
+        dim3 g(static_cast<unsigned>((p.n[2] + 127) / 128), static_cast<unsigned>(p.n[1]),
+               static_cast<unsigned>(p.n[0]));
+        grad_final_kernel<<<g, b, 0, p.stream>>>(p.grad, p.hist + 2 * L, p.v[2 % 3], p.v[1 % 3],
+                                                 p.v[0], p.ac.cm, p.pitch, p.plane,
+                                                 static_cast<int>(p.n[0]),
+                                                 static_cast<int>(p.n[1]),
+                                                 static_cast<int>(p.n[2]), p.ac.radius);
+    }
+    p.ac = p.ac_fwd;
+}
+
+// graph keys: [b, e) step ranges; negative keys for special sequences
+constexpr int64_t kStencilOnly = -1, kFwiForward = -2, kFwiAdjoint = -3;
+
+void enqueue_steps(Plan& p, int64_t b, int64_t e) {
+    if (b == kStencilOnly) {
+        for (int64_t k = 0; k < p.nt; ++k) {
+            if (p.kind == Plan::DIFFUSION)
+                enqueue_diffusion_step(p, k);
+            else
+                enqueue_acoustic_step(p, k, p.slot, true);
+        }
+        return;
+    }
+    if (b == kFwiForward) return enqueue_fwi_forward(p);
+    if (b == kFwiAdjoint) return enqueue_fwi_adjoint(p);
+    for (int64_t k = b; k < e; ++k) {
+        if (p.kind == Plan::DIFFUSION)
+            enqueue_diffusion_step(p, k);
+        else
+            enqueue_acoustic_step(p, k, p.slot);
+    }
+}
+
+// Steps [b, e) as one cached CUDA graph (the OpenMP team + barriers of the
+// generated loop become graph edges; launches cost ~graph-node latency).
+void run_steps(Plan& p, int64_t b, int64_t e) {
+    if (b >= e && b >= 0) return;
+    auto key = std::make_pair(b, e);
+    auto it = p.graphs.find(key);
+    if (it == p.graphs.end()) {
+        cudaGraph_t g = nullptr;
+        SF_CUDA(cudaStreamBeginCapture(p.stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue_steps(p, b, e);
+        } catch (...) {
+            cudaStreamEndCapture(p.stream, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        SF_CUDA(cudaStreamEndCapture(p.stream, &g));
+        cudaGraphExec_t ge = nullptr;
+        SF_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        cudaGraphDestroy(g);
+        it = p.graphs.emplace(key, ge).first;
+    }
+    SF_CUDA(cudaGraphLaunch(it->second, p.stream));
+}
+
+void choose_geometry(Plan& p) {
+    if (p.kind == Plan::DIFFUSION || p.ndim == 2) return;
+    const int r = p.ac.radius;
+    const int TY = 16;
+    p.block3 = dim3(32, TY, 1);
+    const int64_t gx = (p.n[2] + 31) / 32, gy = (p.n[1] + TY - 1) / TY;
+    const int64_t nz = p.n[0] - 2 * r;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
+    // about 4 resident 512-thread CTAs per SM; aim for ~2 waves of CTAs
+    const int64_t target = static_cast<int64_t>(sms) * 8;
+    int64_t gz = std::max<int64_t>(1, (target + gx * gy - 1) / (gx * gy));
+    int64_t zc = std::max<int64_t>((nz + gz - 1) / gz, std::min<int64_t>(nz, 4 * r + 8));
+    gz = (nz + zc - 1) / zc;
+    p.zchunk = static_cast<int>(zc);
+    p.grid3 = dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(gz));
+}
+
+void init_device(Plan& p, int device) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        throw Status(SF_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    if (device < 0 || device >= count) throw Status(SF_ERR_INVALID, "device index out of range");
+    p.device = device;
+    SF_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    SF_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        throw Status(SF_ERR_CUDA, std::string("device ") + prop.name +
+                                      " is not sm_100-class; this library is built for sm_100a");
+    SF_CUDA(cudaStreamCreateWithFlags(&p.stream, cudaStreamNonBlocking));
+    SF_CUDA(cudaEventCreate(&p.ev0));
+    SF_CUDA(cudaEventCreate(&p.ev1));
+}
+
+void layout(Plan& p, int ndim, const int64_t* shape) {
+    p.ndim = ndim;
+    for (int i = 0; i < 3; ++i) p.n[i] = i < ndim ? shape[i] : 1;
+    const int64_t last = shape[ndim - 1];
+    p.pitch = round_up(last, 32);
+    if (ndim == 3) {
+        p.plane = p.n[1] * p.pitch;
+        p.slot_elems = p.n[0] * p.plane;
+    } else {
+        p.plane = 0;
+        p.slot_elems = p.n[0] * p.pitch;
+    }
+    for (int i = 0; i < ndim; ++i)
+        if (shape[i] > (int64_t{1} << 30)) throw Status(SF_ERR_INVALID, "extent too large");
+}
+
+float* alloc_field(Plan& p) {
+    float* f = dalloc<float>(static_cast<size_t>(p.slot_elems));
+    SF_CUDA(cudaMemsetAsync(f, 0, sizeof(float) * p.slot_elems, p.stream));
+    return f;
+}
+
+void check_acoustic_desc(const sf_acoustic_desc* d) {
+    if (!d) throw Status(SF_ERR_INVALID, "null descriptor");
+    if (d->ndim < 2 || d->ndim > 3) throw Status(SF_ERR_INVALID, "acoustic needs 2 or 3 dims");
+    if (d->space_order < 2 || d->space_order > 16 || d->space_order % 2)
+        throw Status(SF_ERR_INVALID, "space_order must be even and >= 2, got " +
+                                         std::to_string(d->space_order));
+    for (int i = 0; i < d->ndim; ++i)
+        if (d->shape[i] < d->space_order + 1)
+            throw Status(SF_ERR_INVALID, "extent " + std::to_string(d->shape[i]) +
+                                             " too small for order " +
+                                             std::to_string(d->space_order));
+    if (d->nt < 0 || d->n_src < 1 || d->n_rec < 1)
+        throw Status(SF_ERR_INVALID, "nt must be >= 0 and point sets non-empty");
+    if (!(d->dt > 0) || !(d->spacing > 0)) throw Status(SF_ERR_INVALID, "dt/spacing must be > 0");
+}
+
+void setup_acoustic(Plan& p, const sf_acoustic_desc* d, int device, bool fwi) {
+    check_acoustic_desc(d);
+    init_device(p, device);
+    layout(p, d->ndim, d->shape);
+    p.nt = d->nt;
+    p.ac = acoustic_constants(d->ndim, d->space_order, fwi ? true : d->forward != 0, d->dt,
+                              d->spacing);
+    p.m = alloc_field(p);
+    p.eta = alloc_field(p);
+    alloc_points(p, p.src, d->n_src, d->nt);
+    alloc_points(p, p.rec, d->n_rec, d->nt);
+    choose_geometry(p);
+    const int corners = 1 << p.ndim;
+    const int64_t fb = field_numel(p) * 4;
+    p.arg_names = {d->forward || fwi ? "u" : "v", "m", "eta", "src", "src_ci", "src_w",
+                   "rec", "rec_ci", "rec_w"};
+    p.arg_bytes = {3 * fb, fb, fb, d->nt * d->n_src * 4, d->n_src * p.ndim * 4,
+                   d->n_src * corners * 4, d->nt * d->n_rec * 4, d->n_rec * p.ndim * 4,
+                   d->n_rec * corners * 4};
+    p.launches_per_step = 3;
+}
+
+void upload_acoustic(Plan& p, void* const* a) {
+    const bool fwd = p.ac.forward;
+    for (int s = 0; s < 3; ++s)
+        if (a[0]) h2d_field(p, p.slot[s], static_cast<const float*>(a[0]) + s * field_numel(p));
+    if (a[1]) h2d_field(p, p.m, static_cast<const float*>(a[1]));
+    if (a[2]) h2d_field(p, p.eta, static_cast<const float*>(a[2]));
+    upload_points(p, p.src, static_cast<const float*>(a[3]), static_cast<const int*>(a[4]),
+                  static_cast<const float*>(a[5]), fwd);
+    upload_points(p, p.rec, static_cast<const float*>(a[6]), static_cast<const int*>(a[7]),
+                  static_cast<const float*>(a[8]), !fwd);
+}
+
+void download_acoustic(Plan& p, void* const* a) {
+    for (int s = 0; s < 3; ++s)
+        if (a[0]) d2h_field(p, static_cast<float*>(a[0]) + s * field_numel(p), p.slot[s]);
+    if (a[1]) d2h_field(p, static_cast<float*>(a[1]), p.m);
+    if (a[2]) d2h_field(p, static_cast<float*>(a[2]), p.eta);
+    if (a[3])
+        SF_CUDA(cudaMemcpyAsync(a[3], p.src.series, sizeof(float) * p.nt * p.src.np,
+                                cudaMemcpyDeviceToHost, p.stream));
+    if (a[6])
+        SF_CUDA(cudaMemcpyAsync(a[6], p.rec.series, sizeof(float) * p.nt * p.rec.np,
+                                cudaMemcpyDeviceToHost, p.stream));
+    // ci / w are read-only for the kernel: nothing to copy back
+    SF_CUDA(cudaStreamSynchronize(p.stream));
+}
+
+void upload_any(Plan& p, void* const* a, int nargs) {
+    if (nargs != static_cast<int>(p.arg_names.size()))
+        throw Status(SF_ERR_SIGNATURE, "expected " + std::to_string(p.arg_names.size()) +
+                                           " buffers, got " + std::to_string(nargs));
+    SF_CUDA(cudaSetDevice(p.device));
+    if (p.kind == Plan::DIFFUSION) {
+        if (a[0])
+            for (int s = 0; s < 2; ++s)
+                h2d_field(p, p.slot[s], static_cast<const float*>(a[0]) + s * field_numel(p));
+    } else {
+        upload_acoustic(p, a);
+    }
+}
+
+void download_any(Plan& p, void* const* a, int nargs) {
+    if (nargs != static_cast<int>(p.arg_names.size()))
+        throw Status(SF_ERR_SIGNATURE, "expected " + std::to_string(p.arg_names.size()) +
+                                           " buffers, got " + std::to_string(nargs));
+    SF_CUDA(cudaSetDevice(p.device));
+    if (p.kind == Plan::DIFFUSION) {
+        if (a[0])
+            for (int s = 0; s < 2; ++s)
+                d2h_field(p, static_cast<float*>(a[0]) + s * field_numel(p), p.slot[s]);
+        SF_CUDA(cudaStreamSynchronize(p.stream));
+    } else {
+        download_acoustic(p, a);
+    }
+}
+
+void check_kernel_errors(Plan& p) {
+    SF_CUDA(cudaGetLastError());
+    cudaError_t e = cudaStreamSynchronize(p.stream);
+    if (e != cudaSuccess)
+        throw Status(SF_ERR_KERNEL, std::string("kernel failed: ") + cudaGetErrorString(e));
+}
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return SF_OK;
+    } catch (const Status& s) {
+        set_error(s.what());
+        return s.code;
+    } catch (const std::invalid_argument& e) {
+        set_error(e.what());
+        return SF_ERR_INVALID;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return SF_ERR_INVALID;
+    }
+}
+
+} // namespace
+} // namespace sfb
+
+sf_plan::~sf_plan() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (float* s : slot) sfb::dfree(s);
+    sfb::dfree(m);
+    sfb::dfree(eta);
+    sfb::free_points(src);
+    sfb::free_points(rec);
+    sfb::dfree(hist);
+    sfb::dfree(grad);
+    for (float* s : v) sfb::dfree(s);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+using sfb::guard;
+using sfb::Status;
+
+extern "C" {
+
+const char* sf_last_error(void) { return sfb::g_error.c_str(); }
+
+int sf_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int sf_acoustic_plan_create(const sf_acoustic_desc* d, int device, sf_plan** out) {
+    if (!out) return SF_ERR_INVALID;
+    *out = nullptr;
+    auto p = std::make_unique<sf_plan>();
+    p->kind = sf_plan::ACOUSTIC;
+    int rc = guard([&] {
+        sfb::setup_acoustic(*p, d, device, false);
+        for (int s = 0; s < 3; ++s) p->slot[s] = sfb::alloc_field(*p);
+        SF_CUDA(cudaStreamSynchronize(p->stream));
+    });
+    if (rc == SF_OK) *out = p.release();
+    return rc;
+}
+
+int sf_diffusion_plan_create(const sf_diffusion_desc* d, int device, sf_plan** out) {
+    if (!out || !d) return SF_ERR_INVALID;
+    *out = nullptr;
+    auto p = std::make_unique<sf_plan>();
+    p->kind = sf_plan::DIFFUSION;
+    int rc = guard([&] {
+        if (d->order < 2 || d->order > 16 || d->order % 2)
+            throw Status(SF_ERR_INVALID, "order must be even in [2, 16]");
+        if (d->nx < d->order + 1 || d->ny < d->order + 1 || d->nt < 0)
+            throw Status(SF_ERR_INVALID, "grid too small for the order");
+        if (d->alpha_den == 0 || d->dx_den == 0 || d->alpha_num <= 0 || d->dx_num <= 0)
+            throw Status(SF_ERR_INVALID, "alpha and dx must be positive rationals");
+        sfb::init_device(*p, device);
+        const int64_t shape[2] = {d->nx, d->ny};
+        sfb::layout(*p, 2, shape);
+        p->nt = d->nt;
+        p->nslots = 2;
+        p->dc = sfb::diffusion_constants(sfb::Rat::make(d->alpha_num, d->alpha_den),
+                                         sfb::Rat::make(d->dx_num, d->dx_den), d->order);
+        for (int s = 0; s < 2; ++s) p->slot[s] = sfb::alloc_field(*p);
+        p->arg_names = {"u"};
+        p->arg_bytes = {2 * d->nx * d->ny * 4};
+        p->launches_per_step = 1;
+        SF_CUDA(cudaStreamSynchronize(p->stream));
+    });
+    if (rc == SF_OK) *out = p.release();
+    return rc;
+}
+
+void sf_plan_destroy(sf_plan* p) { delete p; }
+
+int sf_plan_num_args(const sf_plan* p) { return p ? static_cast<int>(p->arg_names.size()) : 0; }
+
+const char* sf_plan_arg_name(const sf_plan* p, int i) {
+    if (!p || i < 0 || i >= static_cast<int>(p->arg_names.size())) return nullptr;
+    return p->arg_names[i].c_str();
+}
+
+int64_t sf_plan_arg_bytes(const sf_plan* p, int i) {
+    if (!p || i < 0 || i >= static_cast<int>(p->arg_bytes.size())) return -1;
+    return p->arg_bytes[i];
+}
+
+int sf_plan_upload(sf_plan* p, void* const* args, int nargs) {
+    if (!p) return SF_ERR_INVALID;
+    return guard([&] { sfb::upload_any(*p, args, nargs); });
+}
+
+int sf_plan_download(sf_plan* p, void* const* args, int nargs) {
+    if (!p) return SF_ERR_INVALID;
+    return guard([&] { sfb::download_any(*p, args, nargs); });
+}
+
+int sf_plan_run(sf_plan* p, int64_t b, int64_t e) {
+    if (!p) return SF_ERR_INVALID;
+    return guard([&] {
+        if (p->kind == sf_plan::FWI) throw Status(SF_ERR_INVALID, "use sf_fwi_gradient");
+        if (b < 0 || e > p->nt || b > e) throw Status(SF_ERR_INVALID, "step range out of bounds");
+        SF_CUDA(cudaSetDevice(p->device));
+        sfb::run_steps(*p, b, e);
+        SF_CUDA(cudaGetLastError());
+    });
+}
+
+int sf_plan_synchronize(sf_plan* p) {
+    if (!p) return SF_ERR_INVALID;
+    return guard([&] { sfb::check_kernel_errors(*p); });
+}
+
+int sf_plan_invoke(sf_plan* p, void* const* args, int nargs) {
+    if (!p) return SF_ERR_INVALID;
+    return guard([&] {
+        if (p->kind == sf_plan::FWI) throw Status(SF_ERR_INVALID, "use sf_fwi_gradient");
+        for (int i = 0; i < nargs; ++i)
+            if (!args[i]) throw Status(SF_ERR_SIGNATURE, "null buffer for " + p->arg_names.at(i));
+        sfb::upload_any(*p, args, nargs);
+        sfb::run_steps(*p, 0, p->nt);
+        sfb::check_kernel_errors(*p);
+        sfb::download_any(*p, args, nargs);
+    });
+}
+
+int sf_acoustic_apply(sf_plan* p, float* u, float* m, float* eta, float* src, int* src_ci,
+                      float* src_w, float* rec, int* rec_ci, float* rec_w) {
+    if (!p || p->kind != sf_plan::ACOUSTIC) {
+        sfb::set_error("not an acoustic plan");
+        return SF_ERR_SIGNATURE;
+    }
+    void* a[9] = {u, m, eta, src, src_ci, src_w, rec, rec_ci, rec_w};
+    return sf_plan_invoke(p, a, 9);
+}
+
+int sf_diffusion_apply(sf_plan* p, float* u) {
+    if (!p || p->kind != sf_plan::DIFFUSION) {
+        sfb::set_error("not a diffusion plan");
+        return SF_ERR_SIGNATURE;
+    }
+    void* a[1] = {u};
+    return sf_plan_invoke(p, a, 1);
+}
+
+int sf_plan_time(sf_plan* p, float* total_ms, float* stencil_ms, int64_t* launches) {
+    if (!p) return SF_ERR_INVALID;
+    return guard([&] {
+        SF_CUDA(cudaSetDevice(p->device));
+        sfb::run_steps(*p, 0, p->nt);  // make sure the graph exists (warm)
+        SF_CUDA(cudaStreamSynchronize(p->stream));
+        SF_CUDA(cudaEventRecord(p->ev0, p->stream));
+        sfb::run_steps(*p, 0, p->nt);
+        SF_CUDA(cudaEventRecord(p->ev1, p->stream));
+        sfb::check_kernel_errors(*p);
+        float ms = 0;
+        SF_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+        if (total_ms) *total_ms = ms;
+        if (launches) *launches = p->launches_per_step * p->nt;
+        if (stencil_ms) {
+            // same steps with only the stencil launches: their summed duration
+            sfb::run_steps(*p, sfb::kStencilOnly, sfb::kStencilOnly);
+            SF_CUDA(cudaStreamSynchronize(p->stream));
+            SF_CUDA(cudaEventRecord(p->ev0, p->stream));
+            sfb::run_steps(*p, sfb::kStencilOnly, sfb::kStencilOnly);
+            SF_CUDA(cudaEventRecord(p->ev1, p->stream));
+            sfb::check_kernel_errors(*p);
+            SF_CUDA(cudaEventElapsedTime(stencil_ms, p->ev0, p->ev1));
+        }
+    });
+}
+
+int sf_fwi_plan_create(const sf_acoustic_desc* d, int device, sf_plan** out) {
+    if (!out) return SF_ERR_INVALID;
+    *out = nullptr;
+    auto p = std::make_unique<sf_plan>();
+    p->kind = sf_plan::FWI;
+    int rc = guard([&] {
+        if (d && d->ndim != 3) throw Status(SF_ERR_INVALID, "FWI gradient is 3D only");
+        sfb::setup_acoustic(*p, d, device, true);
+        p->ac_fwd = p->ac;
+        p->ac_adj = sfb::acoustic_constants(3, d->space_order, false, d->dt, d->spacing);
+        const int64_t levels = d->nt + 2;
+        p->hist = sfb::dalloc<float>(static_cast<size_t>(levels * p->slot_elems));
+        for (int s = 0; s < 3; ++s) p->v[s] = sfb::alloc_field(*p);
+        p->grad = sfb::alloc_field(*p);
+        p->arg_names.clear();
+        p->arg_bytes.clear();
+        SF_CUDA(cudaStreamSynchronize(p->stream));
+    });
+    if (rc == SF_OK) *out = p.release();
+    return rc;
+}
+
+int sf_fwi_gradient(sf_plan* p, const float* m, const float* eta, const float* src,
+                    const int* src_ci, const float* src_w, const int* rec_ci, const float* rec_w,
+                    const float* residual, float* rec_out, float* grad_out, float* v_out,
+                    float* src_adj_out) {
+    if (!p || p->kind != sf_plan::FWI) return SF_ERR_INVALID;
+    return guard([&] {
+        if (!m || !eta || !src || !src_ci || !src_w || !rec_ci || !rec_w || !residual)
+            throw Status(SF_ERR_SIGNATURE, "null input buffer");
+        SF_CUDA(cudaSetDevice(p->device));
+        sfb::h2d_field(*p, p->m, m);
+        sfb::h2d_field(*p, p->eta, eta);
+        // forward: src injects, rec samples
+        sfb::upload_points(*p, p->src, src, src_ci, src_w, true);
+        sfb::upload_points(*p, p->rec, nullptr, rec_ci, rec_w, true);
+        sfb::run_steps(*p, sfb::kFwiForward, sfb::kFwiForward);
+        sfb::check_kernel_errors(*p);
+        if (rec_out)
+            SF_CUDA(cudaMemcpyAsync(rec_out, p->rec.series, sizeof(float) * p->nt * p->rec.np,
+                                    cudaMemcpyDeviceToHost, p->stream));
+        // adjoint: residual injected at receivers, source positions sampled
+        SF_CUDA(cudaStreamSynchronize(p->stream));
+        SF_CUDA(cudaMemcpyAsync(p->rec.series, residual, sizeof(float) * p->nt * p->rec.np,
+                                cudaMemcpyHostToDevice, p->stream));
+        sfb::run_steps(*p, sfb::kFwiAdjoint, sfb::kFwiAdjoint);
+        sfb::check_kernel_errors(*p);
+        if (grad_out) sfb::d2h_field(*p, grad_out, p->grad);
+        if (v_out)
+            for (int s = 0; s < 3; ++s)
+                sfb::d2h_field(*p, v_out + s * sfb::field_numel(*p), p->v[s]);
+        if (src_adj_out)
+            SF_CUDA(cudaMemcpyAsync(src_adj_out, p->src.series, sizeof(float) * p->nt * p->src.np,
+                                    cudaMemcpyDeviceToHost, p->stream));
+        SF_CUDA(cudaStreamSynchronize(p->stream));
+    });
+}
+
+int sf_fwi_time(sf_plan* p, float* fwd_ms, float* adj_ms) {
+    if (!p || p->kind != sf_plan::FWI) return SF_ERR_INVALID;
+    return guard([&] {
+        SF_CUDA(cudaSetDevice(p->device));
+        SF_CUDA(cudaEventRecord(p->ev0, p->stream));
+        sfb::run_steps(*p, sfb::kFwiForward, sfb::kFwiForward);
+        SF_CUDA(cudaEventRecord(p->ev1, p->stream));
+        sfb::check_kernel_errors(*p);
+        SF_CUDA(cudaEventElapsedTime(fwd_ms, p->ev0, p->ev1));
+        SF_CUDA(cudaEventRecord(p->ev0, p->stream));
+        sfb::run_steps(*p, sfb::kFwiAdjoint, sfb::kFwiAdjoint);
+        SF_CUDA(cudaEventRecord(p->ev1, p->stream));
+        sfb::check_kernel_errors(*p);
+        SF_CUDA(cudaEventElapsedTime(adj_ms, p->ev0, p->ev1));
+    });
+}
+
+int sf_interpolation_weights(int ndim, const double* coord, double spacing,
+                             const int64_t* extents, int32_t* cell, float* w) {
+    if (ndim < 1 || ndim > 3) return SF_ERR_INVALID;
+    return sfb::interpolation_weights(ndim, coord, spacing, extents, cell, w)
+               ? SF_OK
+               : SF_ERR_OUT_OF_DOMAIN;
+}
+
+double sf_stable_dt(int ndim, int order, double spacing, double v_top, double v_bottom) {
+    try {
+        return sfb::stable_dt(ndim, order, spacing, v_top, v_bottom);
+    } catch (const std::exception& e) {
+        sfb::set_error(e.what());
+        return -1.0;
+    }
+}
+
+double sf_ricker(double f0, double t, double t0) { return sfb::ricker(f0, t, t0); }
+
+int sf_build_medium(int ndim, const int64_t* shape, int boundary_width, double spacing,
+                    double v_top, double v_bottom, const double* v_field, double v_min, float* m,
+                    float* eta) {
+    if (ndim < 2 || ndim > 3 || !shape || !m || !eta) return SF_ERR_INVALID;
+    sfb::build_medium(ndim, shape, boundary_width, spacing, v_top, v_bottom, v_field, v_min, m,
+                      eta);
+    return SF_OK;
+}
+
+int sf_acoustic_constants(int ndim, int order, int forward, double dt, double spacing,
+                          float* out, int* tsel) {
+    return guard([&] {
+        sfb::AcousticConstants c = sfb::acoustic_constants(ndim, order, forward != 0, dt, spacing);
+        std::fill(out, out + 15, 0.0f);
+        out[0] = c.ce;
+        out[1] = c.cm;
+        for (int k = 0; k < 3; ++k) {
+            out[2 + k] = c.tc[k];
+            tsel[k] = c.tsel[k];
+        }
+        out[5] = c.c0;
+        for (int j = 0; j < c.radius; ++j) out[6 + j] = c.cj[j];
+        out[14] = c.src_scale;
+    });
+}
+
+int sf_diffusion_constants(int order, int64_t an, int64_t ad, int64_t dn, int64_t dd, float* c0,
+                           int* has_c0, float* cj) {
+    return guard([&] {
+        sfb::DiffusionConstants c =
+            sfb::diffusion_constants(sfb::Rat::make(an, ad), sfb::Rat::make(dn, dd), order);
+        *c0 = c.c0;
+        *has_c0 = c.has_c0;
+        for (int j = 0; j < 8; ++j) cj[j] = c.cj[j];
+    });
+}
+
+} // extern "C"

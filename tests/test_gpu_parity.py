@@ -1,0 +1,284 @@
+"""Parity of the CUDA path (through the C ABI) against the reference.
+
+Bar: bitwise equality of every field slot and sparse trace with the
+reference's generated kernel (the north-star tolerance is relative L2 1e-5
+on fields and traces; the kernels reproduce the reference's fp32 operation
+order, so equality is exact and asserted as such, with the 1e-5 relative L2
+bound checked as well). The checker is the C restatement (oracle/sf_port.c),
+itself pinned to the reference in test_oracle_pin.py, plus golden fixtures
+made by the reference (tests/golden/).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+def rel_l2(a, b):
+    a = a.astype(np.float64)
+    b = b.astype(np.float64)
+    n = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (n if n > 0 else 1.0)
+
+
+def assert_parity(got, want):
+    assert got.shape == want.shape
+    assert rel_l2(got, want) <= 1e-5
+    assert np.array_equal(bits(got), bits(want)), \
+        f"not bitwise: max abs diff {np.abs(got.astype(np.float64) - want).max()}"
+
+
+@pytest.fixture(scope="module")
+def sf():
+    import paper_1609_03361_b200 as sf
+    if sf._lib.lib.sf_device_count() < 1:
+        pytest.fail("no CUDA device: the GPU tests need a B200")
+    return sf
+
+
+def run_plan_raw(sf, shape, order, forward, dt, h, nt, m, eta, src, src_ci, src_w, rec, rec_ci,
+                 rec_w, u=None):
+    """Drive the raw C ABI (sf_acoustic_apply) with dense host buffers."""
+    import ctypes as C
+    from paper_1609_03361_b200 import _lib
+    d = _lib.AcousticDesc()
+    d.ndim = len(shape)
+    for i, e in enumerate(shape):
+        d.shape[i] = e
+    d.space_order, d.forward, d.nt, d.dt, d.spacing = order, int(forward), nt, dt, h
+    d.n_src, d.n_rec = src_ci.shape[0], rec_ci.shape[0]
+    plan = C.c_void_p()
+    sf.api.check(_lib.lib.sf_acoustic_plan_create(C.byref(d), 0, C.byref(plan)))
+    try:
+        u = np.zeros((3,) + tuple(shape), np.float32) if u is None else u
+        bufs = [u, m, eta, src, src_ci, src_w, rec, rec_ci, rec_w]
+        bufs = [np.ascontiguousarray(b) for b in bufs]
+        rc = _lib.lib.sf_acoustic_apply(plan, *[b.ctypes.data for b in bufs])
+        sf.api.check(rc)
+        return bufs
+    finally:
+        _lib.lib.sf_plan_destroy(plan)
+
+
+@pytest.mark.parametrize("tag", ["golden3d_fwd", "o8_3d_adj", "o4_2d_fwd"])
+def test_golden_fields(sf, golden, tag):
+    f = golden["fields"]
+    nt, order, forward, dt, h = f[tag + "_meta"]
+    nt, order, forward = int(nt), int(order), bool(forward)
+    shape = f[tag + "_m"].shape
+    src = f[tag + "_src"].copy() if forward else np.zeros_like(f[tag + "_src"])
+    rec = np.zeros_like(f[tag + "_rec"]) if forward else f[tag + "_residual"].copy()
+    out = run_plan_raw(sf, shape, order, forward, dt, h, nt, f[tag + "_m"], f[tag + "_eta"], src,
+                       f[tag + "_src_ci"], f[tag + "_src_w"], rec, f[tag + "_rec_ci"],
+                       f[tag + "_rec_w"])
+    assert_parity(out[0], f[tag + "_field"])
+    if forward:
+        assert_parity(out[6], f[tag + "_rec"])
+    else:
+        assert_parity(out[3], f[tag + "_src"])
+
+
+@pytest.mark.parametrize("tag", ["diff_o2", "diff_o4"])
+def test_golden_diffusion(sf, golden, tag):
+    from fractions import Fraction
+    f = golden["fields"]
+    n, nt, order, an, ad, dn, dd = (int(x) for x in f[tag + "_meta"])
+    cfg = sf.DiffusionConfig(nx=n, ny=n, alpha=Fraction(an, ad), dx=Fraction(dn, dd),
+                             dy=Fraction(dn, dd), nt=nt, order=order)
+    b = sf.make_diffusion_operator(cfg)
+    b.u.data[0] = f[tag + "_u0"]
+    b.u.data[1] = f[tag + "_u0"]
+    b.op.apply()
+    assert_parity(b.u.data, f[tag + "_out"])
+
+
+def random_case(port, shape, order, seed, nsrc=3, nrec=17, spacing=10.0):
+    rng = np.random.default_rng(seed)
+    nd = len(shape)
+    v = 1500.0 + 3000.0 * rng.random(shape)
+    m, eta = port.medium_from_velocity(v, 5, spacing, 1500.0)
+    dt = min(0.4 * spacing / 4500.0, port.stable_dt(nd, order, spacing, 4500.0, 4500.0))
+    lo = (order // 2 + 1) * spacing
+    def pts(n):
+        return np.stack([rng.uniform(lo, (e - order // 2 - 2) * spacing, n) for e in shape], 1)
+    src_c, rec_c = pts(nsrc), pts(nrec)
+    # force a collision: two sources in the same cell
+    src_c[1] = src_c[0] + 0.1 * spacing * rng.random(nd)
+    src_ci, src_w = port.interp(src_c, spacing, shape)
+    rec_ci, rec_w = port.interp(rec_c, spacing, shape)
+    return dict(m=m, eta=eta, dt=dt, src_ci=src_ci, src_w=src_w, rec_ci=rec_ci, rec_w=rec_w,
+                rng=rng)
+
+
+@pytest.mark.parametrize("order", [2, 4, 6, 8, 10, 12, 14, 16])
+@pytest.mark.parametrize("forward", [True, False])
+def test_acoustic3d_random_medium_vs_oracle(sf, port, order, forward):
+    shape = (37, 45, 70)  # ragged: 70 is not a multiple of 32, 45 not of 16
+    nt = 23
+    c = random_case(port, shape, order, seed=order * 7 + forward)
+    rng = c["rng"]
+    series_src = rng.standard_normal((nt, 3)).astype(np.float32)
+    series_rec = rng.standard_normal((nt, 17)).astype(np.float32)
+    u0 = (1e-3 * rng.standard_normal((3,) + shape)).astype(np.float32)
+    if forward:
+        src, rec = series_src, np.zeros((nt, 17), np.float32)
+    else:
+        src, rec = np.zeros((nt, 3), np.float32), series_rec
+    out = run_plan_raw(sf, shape, order, forward, c["dt"], 10.0, nt, c["m"], c["eta"], src.copy(),
+                       c["src_ci"], c["src_w"], rec.copy(), c["rec_ci"], c["rec_w"], u=u0.copy())
+    coefs = port.coefs(3, order, forward, c["dt"], 10.0)
+    u = u0.copy()
+    if forward:
+        port.acoustic_run(coefs, u, c["m"], c["eta"], src, c["src_ci"], c["src_w"], rec,
+                          c["rec_ci"], c["rec_w"], nt)
+        assert_parity(out[6], rec)
+    else:
+        port.acoustic_run(coefs, u, c["m"], c["eta"], rec, c["rec_ci"], c["rec_w"], src,
+                          c["src_ci"], c["src_w"], nt)
+        assert_parity(out[3], src)
+    assert_parity(out[0], u)
+
+
+@pytest.mark.parametrize("order", [2, 8, 16])
+@pytest.mark.parametrize("forward", [True, False])
+def test_acoustic2d_vs_oracle(sf, port, order, forward):
+    shape = (61, 83)
+    nt = 40
+    c = random_case(port, shape, order, seed=100 + order)
+    rng = c["rng"]
+    src = rng.standard_normal((nt, 3)).astype(np.float32) if forward else np.zeros((nt, 3), np.float32)
+    rec = np.zeros((nt, 17), np.float32) if forward else rng.standard_normal((nt, 17)).astype(np.float32)
+    out = run_plan_raw(sf, shape, order, forward, c["dt"], 10.0, nt, c["m"], c["eta"], src.copy(),
+                       c["src_ci"], c["src_w"], rec.copy(), c["rec_ci"], c["rec_w"])
+    coefs = port.coefs(2, order, forward, c["dt"], 10.0)
+    u = np.zeros((3,) + shape, np.float32)
+    if forward:
+        port.acoustic_run(coefs, u, c["m"], c["eta"], src, c["src_ci"], c["src_w"], rec,
+                          c["rec_ci"], c["rec_w"], nt)
+        assert_parity(out[6], rec)
+    else:
+        port.acoustic_run(coefs, u, c["m"], c["eta"], rec, c["rec_ci"], c["rec_w"], src,
+                          c["src_ci"], c["src_w"], nt)
+        assert_parity(out[3], src)
+    assert_parity(out[0], u)
+
+
+def test_api_forward_matches_live_reference(sf, ref):
+    """acoustic_forward through the mirrored API vs the reference's own
+    acoustic_build + Operator::apply on the same default model."""
+    from oracle_lib import AcousticCase, ref_acoustic
+    model = sf.AcousticModel(shape=(48, 40, 36), nt=40, boundary_width=6, spacing=10.0,
+                             space_order=8)
+    s = sf.acoustic_forward(model)
+    op = ref_acoustic(ref, AcousticCase(shape=(48, 40, 36), nt=40, boundary_width=6,
+                                        spacing=10.0, space_order=8), True)
+    op.apply()
+    assert_parity(s.field.data, op.get("u", np.float32, (3, 48, 40, 36)))
+    assert_parity(s.rec.data.data, op.get("rec", np.float32, (40, 8)))
+
+
+def test_zero_steps_is_identity(sf):
+    model = sf.AcousticModel(shape=(24, 24, 20), nt=0, boundary_width=4)
+    s = sf.acoustic_build(model, True)
+    s.field.data[...] = 1.25
+    s.op.apply()
+    assert np.all(s.field.data == 1.25)
+
+
+def test_zero_source_zero_field(sf):
+    model = sf.AcousticModel(shape=(30, 30, 30), nt=20, boundary_width=4)
+    s = sf.acoustic_forward(model, np.zeros(20))
+    assert not s.field.data.any() and not s.rec.data.data.any()
+
+
+def test_signature_mismatch(sf):
+    model = sf.AcousticModel(shape=(24, 24, 20), nt=2, boundary_width=4)
+    s = sf.acoustic_build(model, True)
+    with pytest.raises(sf.SignatureMismatchError):
+        s.op.apply([s.m] + s.op.args[1:])
+    with pytest.raises(sf.SignatureMismatchError):
+        s.op.apply(s.op.args[:-1])
+
+
+def test_adjoint_dot_test(sf):
+    """Acceptance criterion 5 (acceptance.cpp:208-245) on the GPU path."""
+    for order in (2, 4, 6, 8, 10, 12):
+        m = sf.AcousticModel(shape=(60, 60), nt=250, boundary_width=10, space_order=order)
+        r = sf.adjoint_test(m, 7)
+        assert not r.degenerate and abs(r.ratio - 1.0) <= 1e-5, (order, r)
+    for order in (2, 4):
+        m = sf.AcousticModel(shape=(40, 40, 30), nt=120, boundary_width=8, space_order=order)
+        r = sf.adjoint_test(m, 11)
+        assert not r.degenerate and abs(r.ratio - 1.0) <= 1e-5, (order, r)
+
+
+def test_adjoint_dot_test_matches_reference_products(sf, ref):
+    import ctypes as C
+    ref.lib.sfref_adjoint_test.argtypes = [C.c_int, np.ctypeslib.ndpointer(np.int64), C.c_int,
+                                           C.c_double, C.c_long, C.c_int, C.c_uint,
+                                           np.ctypeslib.ndpointer(np.float64)]
+    out = np.zeros(4)
+    assert ref.lib.sfref_adjoint_test(2, np.array([60, 60], np.int64), 10, 15.0, 100, 4, 7,
+                                      out) == 0
+    r = sf.adjoint_test(sf.AcousticModel(shape=(60, 60), nt=100, boundary_width=10,
+                                         space_order=4), 7)
+    assert r.forward_product == out[0] and r.adjoint_product == out[1]
+
+
+def test_diffusion_config1_layout_and_oracle(sf, port):
+    """Config 1 at full size (2048^2, order 2, exact 1/4 weights) vs the
+    port, bitwise, on a reduced step count."""
+    from fractions import Fraction
+    n, nt = 2048, 60
+    rng = np.random.default_rng(1)
+    u0 = np.zeros((n, n), np.float32)
+    u0[1:-1, 1:-1] = rng.random((n - 2, n - 2))
+    cfg = sf.DiffusionConfig(nx=n, ny=n, alpha=Fraction(1, 2), dx=Fraction(1, 2047),
+                             dy=Fraction(1, 2047), nt=nt, order=2)
+    assert cfg.dt() == Fraction(1, 8380418)
+    b = sf.make_diffusion_operator(cfg)
+    b.u.data[0] = u0
+    b.u.data[1] = u0
+    b.op.apply()
+    u = np.stack([u0, u0])
+    port.diffusion_run(u, 2, (1, 2), (1, 2047), nt)
+    assert_parity(b.u.data, u)
+
+
+def test_fwi_gradient_vs_oracle(sf, port):
+    shape = (34, 30, 40)
+    order, nt = 8, 25
+    c = random_case(port, shape, order, seed=5, nsrc=1, nrec=40)
+    rng = c["rng"]
+    src = rng.standard_normal((nt, 1)).astype(np.float32)
+    residual = rng.standard_normal((nt, 40)).astype(np.float32)
+    plan = sf.FwiPlan(shape, order, nt, c["dt"], 10.0, 1, 40)
+    rec_out, grad, v, srcs = plan.gradient(c["m"], c["eta"], src, c["src_ci"], c["src_w"],
+                                           c["rec_ci"], c["rec_w"], residual, want_v=True,
+                                           want_src=True)
+    cf = port.coefs(3, order, True, c["dt"], 10.0)
+    hist = np.zeros((nt + 2,) + shape, np.float32)
+    rec = np.zeros((nt, 40), np.float32)
+    port.forward_history(cf, hist, c["m"], c["eta"], src, c["src_ci"], c["src_w"], rec,
+                         c["rec_ci"], c["rec_w"], nt)
+    assert_parity(rec_out, rec)
+    # the history run is bitwise the 3-slot forward
+    u = np.zeros((3,) + shape, np.float32)
+    rec2 = np.zeros_like(rec)
+    port.acoustic_run(cf, u, c["m"], c["eta"], src, c["src_ci"], c["src_w"], rec2, c["rec_ci"],
+                      c["rec_w"], nt)
+    assert np.array_equal(bits(hist[nt + 1]), bits(u[nt % 3]))
+    ca = port.coefs(3, order, False, c["dt"], 10.0)
+    vv = np.zeros((3,) + shape, np.float32)
+    g = np.zeros(shape, np.float32)
+    s2 = np.zeros((nt, 1), np.float32)
+    port.adjoint_gradient(ca, vv, c["m"], c["eta"], hist, residual, c["rec_ci"], c["rec_w"], s2,
+                          c["src_ci"], c["src_w"], g, nt)
+    assert_parity(v, vv)
+    assert_parity(srcs, s2)
+    assert np.abs(g).max() > 0
+    assert_parity(grad, g)
