@@ -60,110 +60,161 @@ __device__ __forceinline__ float time_terms(const StencilArgs& A, float temp3, f
 // ---------------------------------------------------------------------------
 // K2/K3: 3D acoustic forward/adjoint update, space order 2R.
 //
-// 2.5D scheme: a CTA owns a 32 x TY tile of (a2, a1) columns and streams
-// along a0 (the slowest axis, depth) over zchunk planes. Each thread keeps
-// the 2R+1 values of its own column along a0 in a register queue, so the a0
-// neighbours cost one coalesced load per plane; the current plane plus
-// R-wide a2/a1 halos are staged in shared memory for the in-plane
-// neighbours. Per point the compulsory DRAM traffic is cur + prev + m + eta
-// reads and one write (20 B); halo re-reads are served by L2.
+// 2.5D scheme. A CTA of 32 x TY threads owns a (32*NX) x TY tile of
+// (a2, a1) columns and streams along a0 (the slowest axis, depth) over
+// zchunk planes. Thread (tx, ty) owns the NX columns a2 = x0 + tx + 32k,
+// k < NX: every global access of a warp is one fully coalesced 128-byte
+// line and the NX accesses of a thread share one address (immediate
+// offsets), which amortises address arithmetic over NX points.
+//  * a0 neighbours: each thread keeps the 2R+1 values of its columns along
+//    a0 in a register queue (one new load per plane);
+//  * a2/a1 neighbours: the current plane plus R-wide halos is staged in a
+//    double-buffered shared-memory tile (one __syncthreads per plane);
+//  * the loads for plane z+1 (queue head, u(t-1), m, eta, halos) are issued
+//    before plane z is computed, so a whole plane of math hides their
+//    latency.
+// Compulsory DRAM traffic per point: u(t), u(t-1), m, eta reads and the
+// u(t+1) write = 20 B; halo re-reads hit L2.
 // GRAD (FWI adjoint): before overwriting the output slot (which holds
 // v(t+2)) accumulate grad += u(t+1) * ((v(t+2) - 2 v(t+1)) + v(t)) * cm.
-template <int R, bool FWD, int TY, bool GRAD>
+template <int R, bool FWD, int TY, int NX, bool GRAD>
 __global__ void __launch_bounds__(32 * TY)
 acoustic3d_kernel(const StencilArgs A) {
-    __shared__ float s[TY + 2 * R][32 + 2 * R];
+    constexpr int W = 32 * NX + 2 * R;  // smem row length
+    constexpr int H = TY + 2 * R;
+    __shared__ float s[2][H][W];
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const int a2 = blockIdx.x * 32 + tx;
+    const int x0 = blockIdx.x * 32 * NX;
     const int a1 = blockIdx.y * TY + ty;
     const int zb = R + blockIdx.z * A.zchunk;
     const int ze = min(zb + A.zchunk, A.n0 - R);
     if (zb >= ze) return;  // uniform per CTA
-    const bool in_arr = a2 < A.n2 && a1 < A.n1;
-    const bool active = in_arr && a2 >= R && a2 < A.n2 - R && a1 >= R && a1 < A.n1 - R;
-    const int64_t col = static_cast<int64_t>(a1) * A.pitch + a2;
 
-    float q[2 * R + 1];
+    bool inarr[NX], active[NX];
 #pragma unroll
-    for (int k = 0; k < 2 * R; ++k)
-        q[k + 1] = in_arr ? __ldg(A.cur + static_cast<int64_t>(zb - R + k) * A.plane + col) : 0.0f;
+    for (int k = 0; k < NX; ++k) {
+        const int a2 = x0 + tx + 32 * k;
+        inarr[k] = a2 < A.n2 && a1 < A.n1;
+        active[k] = inarr[k] && a2 >= R && a2 < A.n2 - R && a1 >= R && a1 < A.n1 - R;
+    }
+    bool any_active = false;
+#pragma unroll
+    for (int k = 0; k < NX; ++k) any_active |= active[k];
 
-    // halo sources for this thread (fixed across planes)
-    const int hl = blockIdx.x * 32 - R + tx;     // a2 of left halo (tx < R)
-    const int hr = blockIdx.x * 32 + 32 + tx;    // a2 of right halo (tx < R)
-    const int vl = blockIdx.y * TY - R + ty;     // a1 of lower halo (ty < R)
-    const int vr = blockIdx.y * TY + TY + ty;    // a1 of upper halo (ty < R)
-    const bool do_hl = tx < R && a1 < A.n1 && hl >= 0;
-    const bool do_hr = tx < R && a1 < A.n1 && hr < A.n2;
-    const bool do_vl = ty < R && a2 < A.n2 && vl >= 0;
-    const bool do_vr = ty < R && a2 < A.n2 && vr < A.n1;
-    const int64_t off_hl = static_cast<int64_t>(a1) * A.pitch + hl;
-    const int64_t off_hr = static_cast<int64_t>(a1) * A.pitch + hr;
-    const int64_t off_vl = static_cast<int64_t>(vl) * A.pitch + a2;
-    const int64_t off_vr = static_cast<int64_t>(vr) * A.pitch + a2;
+    // halo roles: lanes tx < R load the left a2 halo, lanes tx >= 32-R the
+    // right one (row a1); rows ty < R load the a1 halos (columns of the tile)
+    const int hx = tx < R ? x0 - R + tx : x0 + 32 * NX + (tx - (32 - R));
+    const bool do_h = (tx < R || tx >= 32 - R) && a1 < A.n1 && hx >= 0 && hx < A.n2;
+    const int vl = blockIdx.y * TY - R + ty;
+    const int vr = blockIdx.y * TY + TY + ty;
+    bool do_vl[NX], do_vr[NX];
+#pragma unroll
+    for (int k = 0; k < NX; ++k) {
+        const int a2 = x0 + tx + 32 * k;
+        do_vl[k] = ty < R && a2 < A.n2 && vl >= 0;
+        do_vr[k] = ty < R && a2 < A.n2 && vr < A.n1;
+    }
+
+    const int64_t col = static_cast<int64_t>(a1) * A.pitch + x0 + tx;
+    const int64_t hcol = static_cast<int64_t>(a1) * A.pitch + hx;
+    const int64_t vlcol = static_cast<int64_t>(vl) * A.pitch + x0 + tx;
+    const int64_t vrcol = static_cast<int64_t>(vr) * A.pitch + x0 + tx;
+    const int64_t plane = A.plane;
+
+    float q[NX][2 * R + 1];
+#pragma unroll
+    for (int k = 0; k < NX; ++k)
+#pragma unroll
+        for (int j = 0; j < 2 * R; ++j)
+            q[k][j + 1] = inarr[k] ? __ldg(A.cur + (zb - R + j) * plane + col + 32 * k) : 0.0f;
+
+    // prefetched state for the plane about to be staged
+    float qn[NX], pvn[NX], mvn[NX], evn[NX], hn, vln[NX], vrn[NX];
+    float oldn[NX], uhn[NX], gvn[NX];
+    auto prefetch = [&](int z) {
+        const int64_t pz = z * plane;
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            qn[k] = inarr[k] ? __ldg(A.cur + pz + R * plane + col + 32 * k) : 0.0f;
+            pvn[k] = active[k] ? __ldg(A.prev + pz + col + 32 * k) : 0.0f;
+            mvn[k] = active[k] ? __ldg(A.m + pz + col + 32 * k) : 0.0f;
+            evn[k] = active[k] ? __ldg(A.eta + pz + col + 32 * k) : 0.0f;
+            vln[k] = do_vl[k] ? __ldg(A.cur + pz + vlcol + 32 * k) : 0.0f;
+            vrn[k] = do_vr[k] ? __ldg(A.cur + pz + vrcol + 32 * k) : 0.0f;
+            if (GRAD) {
+                oldn[k] = active[k] ? A.out[pz + col + 32 * k] : 0.0f;
+                uhn[k] = active[k] ? __ldg(A.uhist + pz + col + 32 * k) : 0.0f;
+                gvn[k] = active[k] ? A.grad[pz + col + 32 * k] : 0.0f;
+            }
+        }
+        hn = do_h ? __ldg(A.cur + pz + hcol) : 0.0f;
+    };
+    prefetch(zb);
 
     for (int z = zb; z < ze; ++z) {
+        const int b = z & 1;
+        float pv[NX], mv[NX], ev[NX], old[NX], uh[NX], gv[NX];
 #pragma unroll
-        for (int k = 0; k < 2 * R; ++k) q[k] = q[k + 1];
-        const int64_t pz = static_cast<int64_t>(z) * A.plane;
-        q[2 * R] = in_arr ? __ldg(A.cur + pz + static_cast<int64_t>(R) * A.plane + col) : 0.0f;
-        float pv = 0.0f, mv = 0.0f, ev = 0.0f, old = 0.0f, uh = 0.0f, gv = 0.0f;
-        if (active) {
-            pv = __ldg(A.prev + pz + col);
-            mv = __ldg(A.m + pz + col);
-            ev = __ldg(A.eta + pz + col);
+        for (int k = 0; k < NX; ++k) {
+#pragma unroll
+            for (int j = 0; j < 2 * R; ++j) q[k][j] = q[k][j + 1];
+            q[k][2 * R] = qn[k];
+            pv[k] = pvn[k];
+            mv[k] = mvn[k];
+            ev[k] = evn[k];
             if (GRAD) {
-                old = A.out[pz + col];
-                uh = __ldg(A.uhist + pz + col);
-                gv = A.grad[pz + col];
+                old[k] = oldn[k];
+                uh[k] = uhn[k];
+                gv[k] = gvn[k];
+            }
+            s[b][ty + R][tx + R + 32 * k] = q[k][R];
+            if (ty < R) {
+                s[b][ty][tx + R + 32 * k] = vln[k];
+                s[b][ty + TY + R][tx + R + 32 * k] = vrn[k];
             }
         }
-        const float hlv = do_hl ? __ldg(A.cur + pz + off_hl) : 0.0f;
-        const float hrv = do_hr ? __ldg(A.cur + pz + off_hr) : 0.0f;
-        const float vlv = do_vl ? __ldg(A.cur + pz + off_vl) : 0.0f;
-        const float vrv = do_vr ? __ldg(A.cur + pz + off_vr) : 0.0f;
-        __syncthreads();  // previous plane fully consumed
-        s[ty + R][tx + R] = q[R];
-        if (tx < R) {
-            s[ty + R][tx] = hlv;
-            s[ty + R][tx + 32 + R] = hrv;
-        }
-        if (ty < R) {
-            s[ty][tx + R] = vlv;
-            s[ty + TY + R][tx + R] = vrv;
-        }
+        if (tx < R) s[b][ty + R][tx] = hn;
+        if (tx >= 32 - R) s[b][ty + R][32 * NX + R + (tx - (32 - R))] = hn;
         __syncthreads();
-        if (active) {
-            const float cv = q[R];
-            const float temp0 = __fmul_rn(A.ce, ev);
-            const float temp1 = __fmul_rn(A.cm, mv);
-            const float temp2 = __fadd_rn(temp0, temp1);
-            const float temp3 = __fdiv_rn(1.0f, temp2);
-            float acc = time_terms<FWD>(A, temp3, ev, mv, pv, cv);
-            acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(A.c0, temp3), cv));
-            float kc[R];
+        if (z + 1 < ze) prefetch(z + 1);
+        if (any_active) {
+            const int64_t pz = z * plane;
 #pragma unroll
-            for (int j = 0; j < R; ++j) kc[j] = __fmul_rn(A.cj[j], temp3);
-            // last axis (a2): offsets -R..-1, +1..+R
+            for (int k = 0; k < NX; ++k) {
+                if (!active[k]) continue;
+                const float cv = q[k][R];
+                const float temp0 = __fmul_rn(A.ce, ev[k]);
+                const float temp1 = __fmul_rn(A.cm, mv[k]);
+                const float temp2 = __fadd_rn(temp0, temp1);
+                const float temp3 = __fdiv_rn(1.0f, temp2);
+                float acc = time_terms<FWD>(A, temp3, ev[k], mv[k], pv[k], cv);
+                acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(A.c0, temp3), cv));
+                float kc[R];
 #pragma unroll
-            for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], s[ty + R][tx + R - j]));
+                for (int j = 0; j < R; ++j) kc[j] = __fmul_rn(A.cj[j], temp3);
+                const float* row = &s[b][ty + R][tx + R + 32 * k];
+                // last axis (a2): offsets -R..-1, +1..+R
 #pragma unroll
-            for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], s[ty + R][tx + R + j]));
-            // axis 1
+                for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], row[-j]));
 #pragma unroll
-            for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], s[ty + R - j][tx + R]));
+                for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], row[j]));
+                // axis 1
 #pragma unroll
-            for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], s[ty + R + j][tx + R]));
-            // axis 0 (register queue)
+                for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], row[-j * W]));
 #pragma unroll
-            for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], q[R - j]));
+                for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], row[j * W]));
+                // axis 0 (register queue)
 #pragma unroll
-            for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], q[R + j]));
-            if (GRAD) {
-                const float vtt = __fmul_rn(__fadd_rn(__fsub_rn(old, __fmul_rn(2.0f, pv)), cv), A.cm);
-                A.grad[pz + col] = __fadd_rn(gv, __fmul_rn(uh, vtt));
+                for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], q[k][R - j]));
+#pragma unroll
+                for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], q[k][R + j]));
+                if (GRAD) {
+                    const float vtt =
+                        __fmul_rn(__fadd_rn(__fsub_rn(old[k], __fmul_rn(2.0f, pv[k])), cv), A.cm);
+                    A.grad[pz + col + 32 * k] = __fadd_rn(gv[k], __fmul_rn(uh[k], vtt));
+                }
+                A.out[pz + col + 32 * k] = acc;
             }
-            A.out[pz + col] = acc;
         }
     }
 }

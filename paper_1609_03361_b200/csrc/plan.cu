@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -101,8 +102,9 @@ struct sf_plan {
     float* grad = nullptr;
     float* v[3] = {nullptr, nullptr, nullptr};
     // launch geometry
-    dim3 grid3, block3;
+    dim3 grid3;
     int zchunk = 0;
+    int tile_nx = 1, tile_ty = 8;  // 3D stencil tile: (32*tile_nx) x tile_ty
     std::map<std::pair<int64_t, int64_t>, cudaGraphExec_t> graphs;
     std::vector<std::string> arg_names;
     std::vector<int64_t> arg_bytes;
@@ -245,12 +247,28 @@ void upload_points(Plan& p, PointSet& s, const float* series, const int* ci, con
 // ---------------------------------------------------------------------------
 // launch helpers
 
+// Tile shapes compiled for the 3D stencil: TY in {8, 16}; NX (points per
+// thread along a2) up to 4 for R <= 4 and up to 2 above (register queue of
+// NX*(2R+1) floats).
+template <int R, bool FWD, bool GRAD>
+void launch_acoustic3d_t(int nx, int ty, dim3 g, cudaStream_t st, const StencilArgs& A) {
+#define SF_T(NXV, TYV)                                                              \
+    if (nx == NXV && ty == TYV) {                                                   \
+        acoustic3d_kernel<R, FWD, TYV, NXV, GRAD><<<g, dim3(32, TYV), 0, st>>>(A);  \
+        return;                                                                     \
+    }
+    SF_T(1, 8) SF_T(1, 16) SF_T(2, 8) SF_T(2, 16)
+    if constexpr (R <= 4) { SF_T(3, 8) SF_T(3, 16) SF_T(4, 8) SF_T(4, 16) }
+#undef SF_T
+    throw Status(SF_ERR_INVALID, "tile shape not compiled for this order");
+}
+
 template <bool FWD, bool GRAD>
-void launch_acoustic3d_r(int r, dim3 g, dim3 b, cudaStream_t st, const StencilArgs& A) {
+void launch_acoustic3d_r(int r, int nx, int ty, dim3 g, cudaStream_t st, const StencilArgs& A) {
     switch (r) {
 #define SF_CASE(RR)                                                                 \
     case RR:                                                                        \
-        acoustic3d_kernel<RR, FWD, 16, GRAD><<<g, b, 0, st>>>(A);                   \
+        launch_acoustic3d_t<RR, FWD, GRAD>(nx, ty, g, st, A);                        \
         break;
         SF_CASE(1) SF_CASE(2) SF_CASE(3) SF_CASE(4) SF_CASE(5) SF_CASE(6) SF_CASE(7) SF_CASE(8)
 #undef SF_CASE
@@ -315,11 +333,11 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
     const int r = p.ac.radius;
     if (p.ndim == 3) {
         if (grad) {
-            launch_acoustic3d_r<false, true>(r, p.grid3, p.block3, p.stream, A);
+            launch_acoustic3d_r<false, true>(r, p.tile_nx, p.tile_ty, p.grid3, p.stream, A);
         } else if (p.ac.forward) {
-            launch_acoustic3d_r<true, false>(r, p.grid3, p.block3, p.stream, A);
+            launch_acoustic3d_r<true, false>(r, p.tile_nx, p.tile_ty, p.grid3, p.stream, A);
         } else {
-            launch_acoustic3d_r<false, false>(r, p.grid3, p.block3, p.stream, A);
+            launch_acoustic3d_r<false, false>(r, p.tile_nx, p.tile_ty, p.grid3, p.stream, A);
         }
     } else {
         dim3 b(64, 4);
@@ -493,22 +511,54 @@ void run_steps(Plan& p, int64_t b, int64_t e) {
     SF_CUDA(cudaGraphLaunch(it->second, p.stream));
 }
 
-void choose_geometry(Plan& p) {
-    if (p.kind == Plan::DIFFUSION || p.ndim == 2) return;
+int max_tile_nx(int r) { return r <= 4 ? 4 : 2; }
+
+// Grid for the chosen tile: tiles over (a2, a1), chunks over a0 sized for
+// about `waves` full waves of CTAs while keeping chunks long enough that the
+// 2R-plane queue warm-up stays a small overhead.
+void set_grid(Plan& p) {
     const int r = p.ac.radius;
-    const int TY = 16;
-    p.block3 = dim3(32, TY, 1);
-    const int64_t gx = (p.n[2] + 31) / 32, gy = (p.n[1] + TY - 1) / TY;
+    const int64_t wx = 32 * p.tile_nx;
+    const int64_t gx = (p.n[2] + wx - 1) / wx, gy = (p.n[1] + p.tile_ty - 1) / p.tile_ty;
     const int64_t nz = p.n[0] - 2 * r;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
-    // about 4 resident 512-thread CTAs per SM; aim for ~2 waves of CTAs
-    const int64_t target = static_cast<int64_t>(sms) * 8;
+    const int64_t per_sm = p.tile_ty == 16 ? 2 : 4;  // resident CTAs (register-limited)
+    const int64_t target = static_cast<int64_t>(sms) * per_sm * 2;
     int64_t gz = std::max<int64_t>(1, (target + gx * gy - 1) / (gx * gy));
     int64_t zc = std::max<int64_t>((nz + gz - 1) / gz, std::min<int64_t>(nz, 4 * r + 8));
     gz = (nz + zc - 1) / zc;
     p.zchunk = static_cast<int>(zc);
     p.grid3 = dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(gz));
+}
+
+// Default tile: the NX <= max that wastes the fewest lanes on the a2 extent
+// (281 -> NX 3: three 96-wide tiles cover 288), TY 8. SF_TILE="nx,ty"
+// overrides (autotuning experiments).
+void choose_geometry(Plan& p) {
+    if (p.kind == Plan::DIFFUSION || p.ndim == 2) return;
+    const int r = p.ac.radius;
+    int best = 1;
+    int64_t best_cover = INT64_MAX;
+    for (int k = 1; k <= max_tile_nx(r); ++k) {
+        const int64_t w = 32 * k;
+        const int64_t cover = (p.n[2] + w - 1) / w * w;
+        if (cover <= best_cover) {
+            best_cover = cover;
+            best = k;
+        }
+    }
+    p.tile_nx = best;
+    p.tile_ty = 8;
+    if (const char* env = std::getenv("SF_TILE")) {
+        int nx = 0, ty = 0;
+        if (std::sscanf(env, "%d,%d", &nx, &ty) == 2 && nx >= 1 && nx <= max_tile_nx(r) &&
+            (ty == 8 || ty == 16)) {
+            p.tile_nx = nx;
+            p.tile_ty = ty;
+        }
+    }
+    set_grid(p);
 }
 
 void init_device(Plan& p, int device) {
