@@ -84,7 +84,7 @@ def _bind(lib):
     lib.sf_plan_synchronize.argtypes = [_vp]
     lib.sf_plan_time.argtypes = [_vp, C.POINTER(C.c_float), C.POINTER(C.c_float),
                                  C.POINTER(C.c_int64)]
-    lib.sf_fwi_gradient.argtypes = [_vp] * 14
+    lib.sf_fwi_gradient.argtypes = [_vp] * 13
     lib.sf_fwi_time.argtypes = [_vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]
     lib.sf_interpolation_weights.argtypes = [C.c_int, _f64p, C.c_double, _i64p, _i32p, _f32p]
     lib.sf_stable_dt.restype = C.c_double
