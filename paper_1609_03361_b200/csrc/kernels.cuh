@@ -71,12 +71,22 @@ __device__ __forceinline__ float time_terms(const StencilArgs& A, float temp3, f
 //  * a2/a1 neighbours: the current plane plus R-wide halos is staged in a
 //    double-buffered shared-memory tile (one __syncthreads per plane);
 //  * the loads for plane z+1 (queue head, u(t-1), m, eta, halos) are issued
-//    before plane z is computed, so a whole plane of math hides their
-//    latency.
-// Compulsory DRAM traffic per point: u(t), u(t-1), m, eta reads and the
-// u(t+1) write = 20 B; halo re-reads hit L2.
+//    before plane z is computed (two register sets, loop unrolled by two),
+//    so a whole plane of math hides their latency.
+// Addressing is 32-bit element offsets from the field bases (fields are
+// < 2^31 elements), advanced by one plane per step. Fields are allocated
+// with guard slack after the last plane (alloc_field), so every tile load
+// is in bounds and unpredicated; only the stores are masked to the
+// interior. Compulsory DRAM traffic per point: u(t), u(t-1), m, eta reads
+// and the u(t+1) write = 20 B; halo re-reads hit L2.
 // GRAD (FWI adjoint): before overwriting the output slot (which holds
 // v(t+2)) accumulate grad += u(t+1) * ((v(t+2) - 2 v(t+1)) + v(t)) * cm.
+template <int NX, bool GRAD>
+struct PlaneRegs {
+    float q[NX], pv[NX], mv[NX], ev[NX], vl[NX], vr[NX], h;
+    float old[NX], uh[NX], gv[NX];
+};
+
 template <int R, bool FWD, int TY, int NX, bool GRAD>
 __global__ void __launch_bounds__(32 * TY)
 acoustic3d_kernel(const StencilArgs A) {
@@ -90,132 +100,133 @@ acoustic3d_kernel(const StencilArgs A) {
     const int ze = min(zb + A.zchunk, A.n0 - R);
     if (zb >= ze) return;  // uniform per CTA
 
-    bool inarr[NX], active[NX];
+    const int pitch = static_cast<int>(A.pitch);
+    const int plane = static_cast<int>(A.plane);
+    unsigned act = 0;  // bit k: column k is an interior point
 #pragma unroll
     for (int k = 0; k < NX; ++k) {
         const int a2 = x0 + tx + 32 * k;
-        inarr[k] = a2 < A.n2 && a1 < A.n1;
-        active[k] = inarr[k] && a2 >= R && a2 < A.n2 - R && a1 >= R && a1 < A.n1 - R;
+        if (a2 >= R && a2 < A.n2 - R && a1 >= R && a1 < A.n1 - R) act |= 1u << k;
     }
-    bool any_active = false;
-#pragma unroll
-    for (int k = 0; k < NX; ++k) any_active |= active[k];
-
     // halo roles: lanes tx < R load the left a2 halo, lanes tx >= 32-R the
-    // right one (row a1); rows ty < R load the a1 halos (columns of the tile)
-    const int hx = tx < R ? x0 - R + tx : x0 + 32 * NX + (tx - (32 - R));
-    const bool do_h = (tx < R || tx >= 32 - R) && a1 < A.n1 && hx >= 0 && hx < A.n2;
-    const int vl = blockIdx.y * TY - R + ty;
-    const int vr = blockIdx.y * TY + TY + ty;
-    bool do_vl[NX], do_vr[NX];
-#pragma unroll
-    for (int k = 0; k < NX; ++k) {
-        const int a2 = x0 + tx + 32 * k;
-        do_vl[k] = ty < R && a2 < A.n2 && vl >= 0;
-        do_vr[k] = ty < R && a2 < A.n2 && vr < A.n1;
-    }
-
-    const int64_t col = static_cast<int64_t>(a1) * A.pitch + x0 + tx;
-    const int64_t hcol = static_cast<int64_t>(a1) * A.pitch + hx;
-    const int64_t vlcol = static_cast<int64_t>(vl) * A.pitch + x0 + tx;
-    const int64_t vrcol = static_cast<int64_t>(vr) * A.pitch + x0 + tx;
-    const int64_t plane = A.plane;
+    // right one (row a1); warps ty < R load the a1 halo rows of the tile
+    const bool hl = tx < R, hr = tx >= 32 - R, vh = ty < R;
+    const int hxo = hl ? (-R) : (32 * NX - (32 - R));  // a2 offset of this lane's halo
+    const int col = a1 * pitch + x0 + tx;
+    // element offsets relative to `col` of the halo loads of this thread
+    const int o_vl = (blockIdx.y * TY - R + ty - a1) * pitch;   // row a1-halo below
+    const int o_vr = (blockIdx.y * TY + TY + ty - a1) * pitch;  // row a1-halo above
+    const int o_h = hxo;                                         // same row, a2 halo
 
     float q[NX][2 * R + 1];
+    int off = (zb - R) * plane + col;  // offset of plane (zb - R) at this column
 #pragma unroll
-    for (int k = 0; k < NX; ++k)
+    for (int j = 0; j < 2 * R; ++j) {
 #pragma unroll
-        for (int j = 0; j < 2 * R; ++j)
-            q[k][j + 1] = inarr[k] ? __ldg(A.cur + (zb - R + j) * plane + col + 32 * k) : 0.0f;
+        for (int k = 0; k < NX; ++k) q[k][j + 1] = __ldg(A.cur + off + 32 * k);
+        off += plane;
+    }
+    // now off = offset of plane zb + R (the next queue head)
 
-    // prefetched state for the plane about to be staged
-    float qn[NX], pvn[NX], mvn[NX], evn[NX], hn, vln[NX], vrn[NX];
-    float oldn[NX], uhn[NX], gvn[NX];
-    auto prefetch = [&](int z) {
-        const int64_t pz = z * plane;
+    auto prefetch = [&](PlaneRegs<NX, GRAD>& P, int o /* plane z at col */) {
+        const float* c = A.cur + o;
+        const float* qh = A.cur + (o + R * plane);
+        const float* pp = A.prev + o;
+        const float* mp = A.m + o;
+        const float* ep = A.eta + o;
 #pragma unroll
         for (int k = 0; k < NX; ++k) {
-            qn[k] = inarr[k] ? __ldg(A.cur + pz + R * plane + col + 32 * k) : 0.0f;
-            pvn[k] = active[k] ? __ldg(A.prev + pz + col + 32 * k) : 0.0f;
-            mvn[k] = active[k] ? __ldg(A.m + pz + col + 32 * k) : 0.0f;
-            evn[k] = active[k] ? __ldg(A.eta + pz + col + 32 * k) : 0.0f;
-            vln[k] = do_vl[k] ? __ldg(A.cur + pz + vlcol + 32 * k) : 0.0f;
-            vrn[k] = do_vr[k] ? __ldg(A.cur + pz + vrcol + 32 * k) : 0.0f;
-            if (GRAD) {
-                oldn[k] = active[k] ? A.out[pz + col + 32 * k] : 0.0f;
-                uhn[k] = active[k] ? __ldg(A.uhist + pz + col + 32 * k) : 0.0f;
-                gvn[k] = active[k] ? A.grad[pz + col + 32 * k] : 0.0f;
+            P.q[k] = __ldg(qh + 32 * k);
+            P.pv[k] = __ldg(pp + 32 * k);
+            P.mv[k] = __ldg(mp + 32 * k);
+            P.ev[k] = __ldg(ep + 32 * k);
+        }
+        if (GRAD) {
+            const float* op = A.out + o;
+            const float* up = A.uhist + o;
+            const float* gp = A.grad + o;
+#pragma unroll
+            for (int k = 0; k < NX; ++k) {
+                P.old[k] = op[32 * k];
+                P.uh[k] = __ldg(up + 32 * k);
+                P.gv[k] = gp[32 * k];
             }
         }
-        hn = do_h ? __ldg(A.cur + pz + hcol) : 0.0f;
+        if (vh) {
+#pragma unroll
+            for (int k = 0; k < NX; ++k) {
+                P.vl[k] = __ldg(c + o_vl + 32 * k);
+                P.vr[k] = __ldg(c + o_vr + 32 * k);
+            }
+        }
+        if (hl || hr) P.h = __ldg(c + o_h);
     };
-    prefetch(zb);
 
-    for (int z = zb; z < ze; ++z) {
-        const int b = z & 1;
-        float pv[NX], mv[NX], ev[NX], old[NX], uh[NX], gv[NX];
+    auto step = [&](PlaneRegs<NX, GRAD>& P, PlaneRegs<NX, GRAD>& Nx, int z, int o,
+                    float (*sb)[W]) {
 #pragma unroll
         for (int k = 0; k < NX; ++k) {
 #pragma unroll
             for (int j = 0; j < 2 * R; ++j) q[k][j] = q[k][j + 1];
-            q[k][2 * R] = qn[k];
-            pv[k] = pvn[k];
-            mv[k] = mvn[k];
-            ev[k] = evn[k];
-            if (GRAD) {
-                old[k] = oldn[k];
-                uh[k] = uhn[k];
-                gv[k] = gvn[k];
-            }
-            s[b][ty + R][tx + R + 32 * k] = q[k][R];
-            if (ty < R) {
-                s[b][ty][tx + R + 32 * k] = vln[k];
-                s[b][ty + TY + R][tx + R + 32 * k] = vrn[k];
-            }
+            q[k][2 * R] = P.q[k];
+            sb[ty + R][tx + R + 32 * k] = q[k][R];
         }
-        if (tx < R) s[b][ty + R][tx] = hn;
-        if (tx >= 32 - R) s[b][ty + R][32 * NX + R + (tx - (32 - R))] = hn;
-        __syncthreads();
-        if (z + 1 < ze) prefetch(z + 1);
-        if (any_active) {
-            const int64_t pz = z * plane;
+        if (vh) {
 #pragma unroll
             for (int k = 0; k < NX; ++k) {
-                if (!active[k]) continue;
-                const float cv = q[k][R];
-                const float temp0 = __fmul_rn(A.ce, ev[k]);
-                const float temp1 = __fmul_rn(A.cm, mv[k]);
-                const float temp2 = __fadd_rn(temp0, temp1);
-                const float temp3 = __fdiv_rn(1.0f, temp2);
-                float acc = time_terms<FWD>(A, temp3, ev[k], mv[k], pv[k], cv);
-                acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(A.c0, temp3), cv));
-                float kc[R];
-#pragma unroll
-                for (int j = 0; j < R; ++j) kc[j] = __fmul_rn(A.cj[j], temp3);
-                const float* row = &s[b][ty + R][tx + R + 32 * k];
-                // last axis (a2): offsets -R..-1, +1..+R
-#pragma unroll
-                for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], row[-j]));
-#pragma unroll
-                for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], row[j]));
-                // axis 1
-#pragma unroll
-                for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], row[-j * W]));
-#pragma unroll
-                for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], row[j * W]));
-                // axis 0 (register queue)
-#pragma unroll
-                for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], q[k][R - j]));
-#pragma unroll
-                for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], q[k][R + j]));
-                if (GRAD) {
-                    const float vtt =
-                        __fmul_rn(__fadd_rn(__fsub_rn(old[k], __fmul_rn(2.0f, pv[k])), cv), A.cm);
-                    A.grad[pz + col + 32 * k] = __fadd_rn(gv[k], __fmul_rn(uh[k], vtt));
-                }
-                A.out[pz + col + 32 * k] = acc;
+                sb[ty][tx + R + 32 * k] = P.vl[k];
+                sb[ty + TY + R][tx + R + 32 * k] = P.vr[k];
             }
         }
+        if (hl || hr) sb[ty + R][tx + R + hxo] = P.h;
+        __syncthreads();
+        if (z + 1 < ze) prefetch(Nx, o + plane);
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            if (!(act & (1u << k))) continue;
+            const float cv = q[k][R];
+            const float temp0 = __fmul_rn(A.ce, P.ev[k]);
+            const float temp1 = __fmul_rn(A.cm, P.mv[k]);
+            const float temp2 = __fadd_rn(temp0, temp1);
+            const float temp3 = __fdiv_rn(1.0f, temp2);
+            float acc = time_terms<FWD>(A, temp3, P.ev[k], P.mv[k], P.pv[k], cv);
+            acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(A.c0, temp3), cv));
+            float kc[R];
+#pragma unroll
+            for (int j = 0; j < R; ++j) kc[j] = __fmul_rn(A.cj[j], temp3);
+            const float* row = &sb[ty + R][tx + R + 32 * k];
+            // last axis (a2): offsets -R..-1, +1..+R
+#pragma unroll
+            for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], row[-j]));
+#pragma unroll
+            for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], row[j]));
+            // axis 1
+#pragma unroll
+            for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], row[-j * W]));
+#pragma unroll
+            for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], row[j * W]));
+            // axis 0 (register queue)
+#pragma unroll
+            for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], q[k][R - j]));
+#pragma unroll
+            for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], q[k][R + j]));
+            if (GRAD) {
+                const float vtt = __fmul_rn(
+                    __fadd_rn(__fsub_rn(P.old[k], __fmul_rn(2.0f, P.pv[k])), cv), A.cm);
+                A.grad[o + 32 * k] = __fadd_rn(P.gv[k], __fmul_rn(P.uh[k], vtt));
+            }
+            A.out[o + 32 * k] = acc;
+        }
+    };
+
+    PlaneRegs<NX, GRAD> P0, P1;
+    int o = zb * plane + col;
+    prefetch(P0, o);
+    for (int z = zb; z < ze; z += 2) {
+        step(P0, P1, z, o, s[0]);
+        o += plane;
+        if (z + 1 < ze) step(P1, P0, z + 1, o, s[1]);
+        o += plane;
     }
 }
 

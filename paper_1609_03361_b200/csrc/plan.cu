@@ -595,8 +595,14 @@ void layout(Plan& p, int ndim, const int64_t* shape) {
         if (shape[i] > (int64_t{1} << 30)) throw Status(SF_ERR_INVALID, "extent too large");
 }
 
+// Guard slack after every field: the 3D stencil's tile loads are
+// unpredicated, and tiles overhanging the a1/a2 extents read up to one plane
+// past the last plane (never stored). Nothing before the base is touched:
+// every halo read starts at plane >= r.
+int64_t field_slack(const Plan& p) { return (p.ndim == 3 ? p.plane : 0) + 64 * p.pitch + 1024; }
+
 float* alloc_field(Plan& p) {
-    float* f = dalloc<float>(static_cast<size_t>(p.slot_elems));
+    float* f = dalloc<float>(static_cast<size_t>(p.slot_elems + field_slack(p)));
     SF_CUDA(cudaMemsetAsync(f, 0, sizeof(float) * p.slot_elems, p.stream));
     return f;
 }
@@ -905,7 +911,8 @@ int sf_fwi_plan_create(const sf_acoustic_desc* d, int device, sf_plan** out) {
         p->ac_fwd = p->ac;
         p->ac_adj = sfb::acoustic_constants(3, d->space_order, false, d->dt, d->spacing);
         const int64_t levels = d->nt + 2;
-        p->hist = sfb::dalloc<float>(static_cast<size_t>(levels * p->slot_elems));
+        p->hist = sfb::dalloc<float>(
+            static_cast<size_t>(levels * p->slot_elems + sfb::field_slack(*p)));
         for (int s = 0; s < 3; ++s) p->v[s] = sfb::alloc_field(*p);
         p->grad = sfb::alloc_field(*p);
         p->arg_names.clear();
