@@ -105,6 +105,7 @@ struct sf_plan {
     dim3 grid3;
     int zchunk = 0;
     int tile_nx = 1, tile_ty = 8;  // 3D stencil tile: (32*tile_nx) x tile_ty
+    int resident = 0;              // CTAs per SM of the chosen stencil kernel
     std::map<std::pair<int64_t, int64_t>, cudaGraphExec_t> graphs;
     std::vector<std::string> arg_names;
     std::vector<int64_t> arg_bytes;
@@ -261,6 +262,31 @@ void launch_acoustic3d_t(int nx, int ty, dim3 g, cudaStream_t st, const StencilA
     if constexpr (R <= 4) { SF_T(3, 8) SF_T(3, 16) SF_T(4, 8) SF_T(4, 16) }
 #undef SF_T
     throw Status(SF_ERR_INVALID, "tile shape not compiled for this order");
+}
+
+template <int R, bool FWD, bool GRAD>
+const void* acoustic3d_ptr_t(int nx, int ty) {
+#define SF_T(NXV, TYV) \
+    if (nx == NXV && ty == TYV) return reinterpret_cast<const void*>(&acoustic3d_kernel<R, FWD, TYV, NXV, GRAD>);
+    SF_T(1, 8) SF_T(1, 16) SF_T(2, 8) SF_T(2, 16)
+    if constexpr (R <= 4) { SF_T(3, 8) SF_T(3, 16) SF_T(4, 8) SF_T(4, 16) }
+#undef SF_T
+    return nullptr;
+}
+
+template <bool FWD, bool GRAD>
+const void* acoustic3d_ptr(int r, int nx, int ty) {
+    switch (r) {
+        case 1: return acoustic3d_ptr_t<1, FWD, GRAD>(nx, ty);
+        case 2: return acoustic3d_ptr_t<2, FWD, GRAD>(nx, ty);
+        case 3: return acoustic3d_ptr_t<3, FWD, GRAD>(nx, ty);
+        case 4: return acoustic3d_ptr_t<4, FWD, GRAD>(nx, ty);
+        case 5: return acoustic3d_ptr_t<5, FWD, GRAD>(nx, ty);
+        case 6: return acoustic3d_ptr_t<6, FWD, GRAD>(nx, ty);
+        case 7: return acoustic3d_ptr_t<7, FWD, GRAD>(nx, ty);
+        case 8: return acoustic3d_ptr_t<8, FWD, GRAD>(nx, ty);
+        default: return nullptr;
+    }
 }
 
 template <bool FWD, bool GRAD>
@@ -513,9 +539,11 @@ void run_steps(Plan& p, int64_t b, int64_t e) {
 
 int max_tile_nx(int r) { return r <= 4 ? 4 : 2; }
 
-// Grid for the chosen tile: tiles over (a2, a1), chunks over a0 sized for
-// about `waves` full waves of CTAs while keeping chunks long enough that the
-// 2R-plane queue warm-up stays a small overhead.
+// Grid for the chosen tile: tiles over (a2, a1) and chunks over a0. The
+// chunk count is picked with a small cost model: CTAs run in waves of
+// (#SM x resident CTAs/SM), each CTA costs its chunk length plus the 2R-plane
+// queue warm-up, so minimise waves(gz) * (chunk(gz) + 2R) over the chunkings
+// that put at least one full wave on the machine.
 void set_grid(Plan& p) {
     const int r = p.ac.radius;
     const int64_t wx = 32 * p.tile_nx;
@@ -523,13 +551,30 @@ void set_grid(Plan& p) {
     const int64_t nz = p.n[0] - 2 * r;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
-    const int64_t per_sm = p.tile_ty == 16 ? 2 : 4;  // resident CTAs (register-limited)
-    const int64_t target = static_cast<int64_t>(sms) * per_sm * 2;
-    int64_t gz = std::max<int64_t>(1, (target + gx * gy - 1) / (gx * gy));
-    int64_t zc = std::max<int64_t>((nz + gz - 1) / gz, std::min<int64_t>(nz, 4 * r + 8));
-    gz = (nz + zc - 1) / zc;
+    int per_sm = 0;
+    const void* fn = p.ac.forward ? acoustic3d_ptr<true, false>(r, p.tile_nx, p.tile_ty)
+                                  : acoustic3d_ptr<false, false>(r, p.tile_nx, p.tile_ty);
+    if (fn) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.tile_ty, 0);
+    if (per_sm < 1) per_sm = 1;
+    p.resident = per_sm;
+    const int64_t slots = static_cast<int64_t>(sms) * per_sm;
+    double best_cost = 1e30;
+    int64_t best_gz = 1;
+    for (int64_t gz = 1; gz <= nz; ++gz) {
+        const int64_t zc = (nz + gz - 1) / gz;
+        if (gz > 1 && zc < std::min<int64_t>(nz, 2 * r + 6)) break;
+        if (gx * gy * gz < slots && (nz + gz) / (gz + 1) >= 2 * r + 6) continue;  // fill every SM
+        const int64_t waves = (gx * gy * gz + slots - 1) / slots;
+        const double cost = static_cast<double>(waves) * static_cast<double>(zc + 2 * r);
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best_gz = gz;
+        }
+    }
+    const int64_t zc = (nz + best_gz - 1) / best_gz;
     p.zchunk = static_cast<int>(zc);
-    p.grid3 = dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(gz));
+    p.grid3 = dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy),
+                   static_cast<unsigned>((nz + zc - 1) / zc));
 }
 
 // Default tile: the NX <= max that wastes the fewest lanes on the a2 extent
