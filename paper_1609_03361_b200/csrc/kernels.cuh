@@ -87,17 +87,8 @@ struct PlaneRegs {
     float old[NX], uh[NX], gv[NX];
 };
 
-// Occupancy target: 3 CTAs of 256 threads per SM (<= 80 registers) where
-// the register queue is small enough to fit without spilling (measured with
-// -Xptxas -v), else whatever the compiler needs.
-template <int R, int TY, int NX, bool GRAD>
-constexpr int stencil_min_blocks() {
-    return (TY == 8 && !GRAD && NX <= 3 && NX * (2 * R + 1) <= 18 && !(NX == 3 && R >= 2)) ? 3
-                                                                                         : 1;
-}
-
 template <int R, bool FWD, int TY, int NX, bool GRAD>
-__global__ void __launch_bounds__(32 * TY, (stencil_min_blocks<R, TY, NX, GRAD>()))
+__global__ void __launch_bounds__(32 * TY)
 acoustic3d_kernel(const StencilArgs A) {
     constexpr int W = 32 * NX + 2 * R;  // smem row length
     constexpr int H = TY + 2 * R;
