@@ -22,7 +22,10 @@
 #include <vector>
 
 #include "../../include/sf_b200.h"
+#include <cudaTypedefs.h>
+
 #include "kernels.cuh"
+#include "tma_stencil.cuh"
 #include "sf_internal.h"
 
 namespace sfb {
@@ -106,6 +109,11 @@ struct sf_plan {
     int zchunk = 0;
     int tile_nx = 1, tile_ty = 8;  // 3D stencil tile: (32*tile_nx) x tile_ty
     int resident = 0;              // CTAs per SM of the chosen stencil kernel
+    // TMA pipeline path (3D forward/adjoint without the FWI gradient)
+    bool use_tma = false;
+    int tma_stages = 4;
+    size_t tma_smem = 0;
+    CUtensorMap tm_cur[3], tm_pme[3], tm_m, tm_eta;
     std::map<std::pair<int64_t, int64_t>, cudaGraphExec_t> graphs;
     std::vector<std::string> arg_names;
     std::vector<int64_t> arg_bytes;
@@ -303,6 +311,135 @@ void launch_acoustic3d_r(int r, int nx, int ty, dim3 g, cudaStream_t st, const S
     }
 }
 
+// ---- TMA path ------------------------------------------------------------
+int tma_max_nx(int r) { return r <= 4 ? 4 : 2; }
+
+template <int R, bool FWD>
+const void* tma_ptr_t(int nx) {
+    switch (nx) {
+        case 1: return reinterpret_cast<const void*>(&acoustic3d_tma_kernel<R, FWD, 8, 1>);
+        case 2: return reinterpret_cast<const void*>(&acoustic3d_tma_kernel<R, FWD, 8, 2>);
+        case 3:
+            if constexpr (R <= 4) return reinterpret_cast<const void*>(&acoustic3d_tma_kernel<R, FWD, 8, 3>);
+            return nullptr;
+        case 4:
+            if constexpr (R <= 4) return reinterpret_cast<const void*>(&acoustic3d_tma_kernel<R, FWD, 8, 4>);
+            return nullptr;
+        default: return nullptr;
+    }
+}
+
+template <bool FWD>
+const void* tma_ptr(int r, int nx) {
+    switch (r) {
+        case 1: return tma_ptr_t<1, FWD>(nx);
+        case 2: return tma_ptr_t<2, FWD>(nx);
+        case 3: return tma_ptr_t<3, FWD>(nx);
+        case 4: return tma_ptr_t<4, FWD>(nx);
+        case 5: return tma_ptr_t<5, FWD>(nx);
+        case 6: return tma_ptr_t<6, FWD>(nx);
+        case 7: return tma_ptr_t<7, FWD>(nx);
+        case 8: return tma_ptr_t<8, FWD>(nx);
+        default: return nullptr;
+    }
+}
+
+size_t tma_smem_bytes(int r, int nx, int stages) {
+    const int wb = (32 * nx + 2 * r + 3) / 4 * 4;
+    const int cur = (wb * (8 + 2 * r) * 4 + 127) / 128 * 128;
+    const int pme = (32 * nx * 8 * 4 + 127) / 128 * 128;
+    return 256 + static_cast<size_t>(2 * r + stages) * cur + static_cast<size_t>(stages) * 3 * pme;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        SF_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !ptr)
+            throw Status(SF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+// 3D map over one padded field: dims (n2, n1, n0), row/plane strides in
+// bytes (multiples of 16 by the 32-float pitch), box (bx, by, 1).
+void make_tensor_map(CUtensorMap* map, const Plan& p, const float* base, uint32_t bx, uint32_t by) {
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.n[2]), static_cast<cuuint64_t>(p.n[1]),
+                          static_cast<cuuint64_t>(p.n[0])};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.pitch) * 4,
+                             static_cast<cuuint64_t>(p.plane) * 4};
+    cuuint32_t box[3] = {bx, by, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                                      const_cast<float*>(base), dims, strides, box, es,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw Status(SF_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+
+void setup_tma(Plan& p) {
+    const int r = p.ac.radius;
+    const int nx = p.tile_nx;
+    const uint32_t wb = static_cast<uint32_t>((32 * nx + 2 * r + 3) / 4 * 4);
+    for (int s = 0; s < 3; ++s) {
+        make_tensor_map(&p.tm_cur[s], p, p.slot[s], wb, static_cast<uint32_t>(8 + 2 * r));
+        make_tensor_map(&p.tm_pme[s], p, p.slot[s], static_cast<uint32_t>(32 * nx), 8);
+    }
+    make_tensor_map(&p.tm_m, p, p.m, static_cast<uint32_t>(32 * nx), 8);
+    make_tensor_map(&p.tm_eta, p, p.eta, static_cast<uint32_t>(32 * nx), 8);
+    // deepest pipeline that still lets 2 CTAs share an SM
+    int stages = 6;
+    while (stages > 2 && tma_smem_bytes(r, nx, stages) * 2 > 220 * 1024) --stages;
+    if (const char* env = std::getenv("SF_TMA_STAGES")) {
+        const int v = std::atoi(env);
+        if (v >= 2 && v <= 16) stages = v;
+    }
+    p.tma_stages = stages;
+    p.tma_smem = tma_smem_bytes(r, nx, stages);
+    for (int fwd = 0; fwd < 2; ++fwd) {
+        const void* fn = fwd ? tma_ptr<true>(r, nx) : tma_ptr<false>(r, nx);
+        if (!fn) throw Status(SF_ERR_INVALID, "TMA tile not compiled");
+        SF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(p.tma_smem)));
+    }
+}
+
+template <int R, bool FWD>
+void launch_tma_t(int nx, dim3 g, size_t smem, cudaStream_t st, const TmaStencilArgs& A) {
+    dim3 b(32, 8);
+    switch (nx) {
+        case 1: acoustic3d_tma_kernel<R, FWD, 8, 1><<<g, b, smem, st>>>(A); return;
+        case 2: acoustic3d_tma_kernel<R, FWD, 8, 2><<<g, b, smem, st>>>(A); return;
+        case 3:
+            if constexpr (R <= 4) { acoustic3d_tma_kernel<R, FWD, 8, 3><<<g, b, smem, st>>>(A); return; }
+            break;
+        case 4:
+            if constexpr (R <= 4) { acoustic3d_tma_kernel<R, FWD, 8, 4><<<g, b, smem, st>>>(A); return; }
+            break;
+    }
+    throw Status(SF_ERR_INVALID, "TMA tile not compiled");
+}
+
+template <bool FWD>
+void launch_tma(int r, int nx, dim3 g, size_t smem, cudaStream_t st, const TmaStencilArgs& A) {
+    switch (r) {
+        case 1: return launch_tma_t<1, FWD>(nx, g, smem, st, A);
+        case 2: return launch_tma_t<2, FWD>(nx, g, smem, st, A);
+        case 3: return launch_tma_t<3, FWD>(nx, g, smem, st, A);
+        case 4: return launch_tma_t<4, FWD>(nx, g, smem, st, A);
+        case 5: return launch_tma_t<5, FWD>(nx, g, smem, st, A);
+        case 6: return launch_tma_t<6, FWD>(nx, g, smem, st, A);
+        case 7: return launch_tma_t<7, FWD>(nx, g, smem, st, A);
+        case 8: return launch_tma_t<8, FWD>(nx, g, smem, st, A);
+        default: throw Status(SF_ERR_INVALID, "radius out of range");
+    }
+}
+
 template <bool FWD>
 void launch_acoustic2d_r(int r, dim3 g, dim3 b, cudaStream_t st, const StencilArgs& A) {
     switch (r) {
@@ -351,8 +488,43 @@ StencilArgs stencil_args(const Plan& p, float* out, const float* cur, const floa
     return A;
 }
 
+int slot_index(const Plan& p, const float* f) {
+    for (int s = 0; s < 3; ++s)
+        if (p.slot[s] == f) return s;
+    return -1;
+}
+
 void launch_stencil(const Plan& p, float* out, const float* cur, const float* prev,
                     float* grad = nullptr, const float* uhist = nullptr) {
+    if (p.use_tma && !grad && p.ndim == 3) {
+        const int sc = slot_index(p, cur), sp = slot_index(p, prev);
+        if (sc >= 0 && sp >= 0) {
+            TmaStencilArgs T;
+            std::memset(&T, 0, sizeof T);
+            T.cur = p.tm_cur[sc];
+            T.prev = p.tm_pme[sp];
+            T.m = p.tm_m;
+            T.eta = p.tm_eta;
+            T.out = out;
+            T.pitch = static_cast<int>(p.pitch);
+            T.plane = static_cast<int>(p.plane);
+            T.n0 = static_cast<int>(p.n[0]);
+            T.n1 = static_cast<int>(p.n[1]);
+            T.n2 = static_cast<int>(p.n[2]);
+            T.zchunk = p.zchunk;
+            T.stages = p.tma_stages;
+            T.ce = p.ac.ce;
+            T.cm = p.ac.cm;
+            for (int k = 0; k < 3; ++k) T.tc[k] = p.ac.tc[k];
+            T.c0 = p.ac.c0;
+            for (int j = 0; j < 8; ++j) T.cj[j] = p.ac.cj[j];
+            if (p.ac.forward)
+                launch_tma<true>(p.ac.radius, p.tile_nx, p.grid3, p.tma_smem, p.stream, T);
+            else
+                launch_tma<false>(p.ac.radius, p.tile_nx, p.grid3, p.tma_smem, p.stream, T);
+            return;
+        }
+    }
     StencilArgs A = stencil_args(p, out, cur, prev);
     A.grad = grad;
     A.uhist = uhist;
@@ -552,9 +724,14 @@ void set_grid(Plan& p) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
     int per_sm = 0;
-    const void* fn = p.ac.forward ? acoustic3d_ptr<true, false>(r, p.tile_nx, p.tile_ty)
-                                  : acoustic3d_ptr<false, false>(r, p.tile_nx, p.tile_ty);
-    if (fn) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.tile_ty, 0);
+    if (p.use_tma) {
+        const void* fn = p.ac.forward ? tma_ptr<true>(r, p.tile_nx) : tma_ptr<false>(r, p.tile_nx);
+        if (fn) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, p.tma_smem);
+    } else {
+        const void* fn = p.ac.forward ? acoustic3d_ptr<true, false>(r, p.tile_nx, p.tile_ty)
+                                      : acoustic3d_ptr<false, false>(r, p.tile_nx, p.tile_ty);
+        if (fn) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.tile_ty, 0);
+    }
     if (per_sm < 1) per_sm = 1;
     p.resident = per_sm;
     const int64_t slots = static_cast<int64_t>(sms) * per_sm;
@@ -603,6 +780,18 @@ void choose_geometry(Plan& p) {
             p.tile_ty = ty;
         }
     }
+    set_grid(p);
+}
+
+// Switch a 3D plan to the TMA pipeline once its slots exist (SF_NO_TMA=1
+// keeps the per-thread-load kernel, for comparisons).
+void enable_tma(Plan& p) {
+    if (p.ndim != 3) return;
+    if (const char* env = std::getenv("SF_NO_TMA"))
+        if (env[0] == '1') return;
+    if (p.ac.radius > 4 && !std::getenv("SF_TILE")) p.tile_nx = 1;
+    setup_tma(p);
+    p.use_tma = true;
     set_grid(p);
 }
 
@@ -811,6 +1000,7 @@ int sf_acoustic_plan_create(const sf_acoustic_desc* d, int device, sf_plan** out
     int rc = guard([&] {
         sfb::setup_acoustic(*p, d, device, false);
         for (int s = 0; s < 3; ++s) p->slot[s] = sfb::alloc_field(*p);
+        sfb::enable_tma(*p);
         SF_CUDA(cudaStreamSynchronize(p->stream));
     });
     if (rc == SF_OK) *out = p.release();

@@ -1,0 +1,235 @@
+// tma_stencil.cuh — TMA/mbarrier-pipelined 3D acoustic stencil (sm_100a).
+//
+// Same arithmetic contract as kernels.cuh (the reference's emitted fp32
+// expression, operation for operation). What changes is how data reaches
+// the SM: instead of per-thread loads, one elected thread drives the Tensor
+// Memory Accelerator, which streams 3D boxes of every input plane into a
+// shared-memory pipeline S planes ahead of the compute:
+//
+//   cur ring  : 2R+S slots, each the (32*NX + 2R) x (TY + 2R) box of u(t) at
+//               one a0 plane, halo included (TMA zero-fills out-of-range
+//               boxes at the grid faces, which only feed non-stored points);
+//               the a0 neighbours of plane z are the same (a1, a2) position
+//               in the slots of planes z-R..z+R, so no register queue;
+//   pme stage : S slots of the (32*NX) x TY boxes of u(t-1), m, eta.
+//
+// Group i (iteration z = zb + i) = cur plane z+R + the u(t-1)/m/eta boxes of
+// plane z, completing on mbarrier i % S (expect_tx = its byte count). After
+// computing plane z every thread passes one __syncthreads; thread 0 then
+// re-arms that barrier and issues group i+S into the slots just released
+// (cur plane z-R, pme slot of z). Loads cost no registers and no LSU issue
+// slots, so warps only spend issue bandwidth on the math and the LDS of the
+// neighbours; the output is written with coalesced 128-byte stores.
+#pragma once
+
+#include <cuda.h>
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace sfb {
+
+struct TmaStencilArgs {
+    CUtensorMap cur;   // box (WB, TY+2R, 1) at (x0-R, y0-R, z)
+    CUtensorMap prev;  // box (32*NX, TY, 1)
+    CUtensorMap m;     // box (32*NX, TY, 1)
+    CUtensorMap eta;   // box (32*NX, TY, 1)
+    float* out;
+    int pitch, plane;  // elements
+    int n0, n1, n2;
+    int zchunk;
+    int stages;
+    float ce, cm;
+    float tc[3];
+    float c0;
+    float cj[8];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "SF_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra SF_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int R, int NX>
+struct TmaBox {
+    static constexpr int WB = (32 * NX + 2 * R + 3) / 4 * 4;  // 16-byte multiple rows
+};
+
+template <int R, int TY, int NX>
+struct TmaLayout {
+    static constexpr int WB = TmaBox<R, NX>::WB;
+    static constexpr int H = TY + 2 * R;
+    static constexpr int CUR_FLOATS = WB * H;
+    static constexpr int CUR_BYTES = (CUR_FLOATS * 4 + 127) / 128 * 128;
+    static constexpr int PME_FLOATS = 32 * NX * TY;
+    static constexpr int PME_BYTES = (PME_FLOATS * 4 + 127) / 128 * 128;
+    static constexpr int BAR_BYTES = 256;  // up to 31 stages + prologue barrier
+    static constexpr size_t smem(int stages) {
+        return BAR_BYTES + static_cast<size_t>(2 * R + stages) * CUR_BYTES +
+               static_cast<size_t>(stages) * 3 * PME_BYTES;
+    }
+};
+
+template <int R, bool FWD, int TY, int NX>
+__global__ void __launch_bounds__(32 * TY) acoustic3d_tma_kernel(const __grid_constant__ TmaStencilArgs A) {
+    using L = TmaLayout<R, TY, NX>;
+    constexpr int WB = L::WB;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    unsigned char* cur_base = smem + L::BAR_BYTES;
+    const int S = A.stages;
+    const int NR = 2 * R + S;
+    unsigned char* pme_base = cur_base + static_cast<size_t>(NR) * L::CUR_BYTES;
+
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = ty * 32 + tx;
+    const int x0 = blockIdx.x * 32 * NX;
+    const int y0 = blockIdx.y * TY;
+    const int zb = R + blockIdx.z * A.zchunk;
+    const int ze = min(zb + A.zchunk, A.n0 - R);
+    if (zb >= ze) return;  // uniform per CTA
+    const int nit = ze - zb;
+
+    auto cur_slot = [&](int p) {  // smem tile of cur plane p (zb-R <= p)
+        return reinterpret_cast<float*>(cur_base + ((p - zb + R) % NR) * L::CUR_BYTES);
+    };
+    auto pme_slot = [&](int i, int f) {
+        return reinterpret_cast<float*>(pme_base + ((i % S) * 3 + f) * L::PME_BYTES);
+    };
+    constexpr uint32_t group_bytes = L::CUR_FLOATS * 4 + 3 * L::PME_FLOATS * 4;
+    auto issue_group = [&](int i) {
+        uint64_t* b = &bar[i % S];
+        const int z = zb + i;
+        mbar_arrive_expect_tx(b, group_bytes);
+        tma_load_3d(cur_slot(z + R), &A.cur, x0 - R, y0 - R, z + R, b);
+        tma_load_3d(pme_slot(i, 0), &A.prev, x0, y0, z, b);
+        tma_load_3d(pme_slot(i, 1), &A.m, x0, y0, z, b);
+        tma_load_3d(pme_slot(i, 2), &A.eta, x0, y0, z, b);
+    };
+
+    if (tid == 0) {
+        for (int i = 0; i <= S; ++i) mbar_init(&bar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        // prologue: planes zb-R .. zb+R-1 of cur on the extra barrier
+        mbar_arrive_expect_tx(&bar[S], 2 * R * L::CUR_FLOATS * 4);
+        for (int j = 0; j < 2 * R; ++j)
+            tma_load_3d(cur_slot(zb - R + j), &A.cur, x0 - R, y0 - R, zb - R + j, &bar[S]);
+        for (int i = 0; i < S && i < nit; ++i) issue_group(i);
+    }
+
+    unsigned act = 0;
+#pragma unroll
+    for (int k = 0; k < NX; ++k) {
+        const int a2 = x0 + tx + 32 * k;
+        const int a1 = y0 + ty;
+        if (a2 >= R && a2 < A.n2 - R && a1 >= R && a1 < A.n1 - R) act |= 1u << k;
+    }
+    const int cpos = (ty + R) * WB + tx + R;  // centre of column k=0 in a cur tile
+    const int ppos = ty * 32 * NX + tx;
+    float* outp = A.out + static_cast<int64_t>(zb) * A.plane +
+                  static_cast<int64_t>(y0 + ty) * A.pitch + x0 + tx;
+
+    mbar_wait(&bar[S], 0);
+    int ring0 = 0;              // ring slot of plane z-R  (= i mod NR)
+    int stage = 0, phase = 0;   // i mod S, (i / S) & 1
+    for (int i = 0; i < nit; ++i) {
+        mbar_wait(&bar[stage], phase);
+        const float* ring[2 * R + 1];  // tiles of planes z-R .. z+R
+#pragma unroll
+        for (int j = 0; j <= 2 * R; ++j) {
+            int sl = ring0 + j;
+            sl = sl >= NR ? sl - NR : sl;
+            ring[j] = reinterpret_cast<const float*>(cur_base + sl * L::CUR_BYTES);
+        }
+        const float* pc = ring[R];
+        const float* pp = reinterpret_cast<const float*>(pme_base + (stage * 3 + 0) * L::PME_BYTES);
+        const float* pm = reinterpret_cast<const float*>(pme_base + (stage * 3 + 1) * L::PME_BYTES);
+        const float* pe = reinterpret_cast<const float*>(pme_base + (stage * 3 + 2) * L::PME_BYTES);
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            if (!(act & (1u << k))) continue;
+            const int c = cpos + 32 * k;
+            const float cv = pc[c];
+            const float pv = pp[ppos + 32 * k];
+            const float mv = pm[ppos + 32 * k];
+            const float ev = pe[ppos + 32 * k];
+            const float temp0 = __fmul_rn(A.ce, ev);
+            const float temp1 = __fmul_rn(A.cm, mv);
+            const float temp2 = __fadd_rn(temp0, temp1);
+            const float temp3 = __fdiv_rn(1.0f, temp2);
+            float acc;
+            {
+                acc = __fmul_rn(__fmul_rn(__fmul_rn(A.tc[0], temp3), ev), pv);
+                if (FWD) {
+                    acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(__fmul_rn(A.tc[1], temp3), mv), pv));
+                    acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(__fmul_rn(A.tc[2], temp3), mv), cv));
+                } else {
+                    acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(__fmul_rn(A.tc[1], temp3), mv), cv));
+                    acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(__fmul_rn(A.tc[2], temp3), mv), pv));
+                }
+            }
+            acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(A.c0, temp3), cv));
+            float kc[R];
+#pragma unroll
+            for (int j = 0; j < R; ++j) kc[j] = __fmul_rn(A.cj[j], temp3);
+            // last axis (a2): offsets -R..-1, +1..+R
+#pragma unroll
+            for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], pc[c - j]));
+#pragma unroll
+            for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], pc[c + j]));
+            // axis 1
+#pragma unroll
+            for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], pc[c - j * WB]));
+#pragma unroll
+            for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], pc[c + j * WB]));
+            // axis 0: same position in the tiles of planes z-R..z+R
+#pragma unroll
+            for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], ring[R - j][c]));
+#pragma unroll
+            for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(kc[j - 1], ring[R + j][c]));
+            outp[32 * k] = acc;
+        }
+        outp += A.plane;
+        __syncthreads();  // every thread is done with cur plane z-R and pme slot i
+        if (tid == 0 && i + S < nit) issue_group(i + S);
+        ring0 = ring0 + 1 == NR ? 0 : ring0 + 1;
+        if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+        }
+    }
+}
+
+} // namespace sfb
