@@ -344,8 +344,10 @@ const void* tma_ptr(int r, int nx) {
     }
 }
 
+int tma_box_width(int r, int nx) { return 32 * nx + 2 * ((r + 3) / 4 * 4); }
+
 size_t tma_smem_bytes(int r, int nx, int stages) {
-    const int wb = (32 * nx + 2 * r + 3) / 4 * 4;
+    const int wb = tma_box_width(r, nx);
     const int cur = (wb * (8 + 2 * r) * 4 + 127) / 128 * 128;
     const int pme = (32 * nx * 8 * 4 + 127) / 128 * 128;
     return 256 + static_cast<size_t>(2 * r + stages) * cur + static_cast<size_t>(stages) * 3 * pme;
@@ -385,7 +387,7 @@ void make_tensor_map(CUtensorMap* map, const Plan& p, const float* base, uint32_
 void setup_tma(Plan& p) {
     const int r = p.ac.radius;
     const int nx = p.tile_nx;
-    const uint32_t wb = static_cast<uint32_t>((32 * nx + 2 * r + 3) / 4 * 4);
+    const uint32_t wb = static_cast<uint32_t>(tma_box_width(r, nx));
     for (int s = 0; s < 3; ++s) {
         make_tensor_map(&p.tm_cur[s], p, p.slot[s], wb, static_cast<uint32_t>(8 + 2 * r));
         make_tensor_map(&p.tm_pme[s], p, p.slot[s], static_cast<uint32_t>(32 * nx), 8);

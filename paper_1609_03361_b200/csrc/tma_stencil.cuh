@@ -6,7 +6,7 @@
 // Memory Accelerator, which streams 3D boxes of every input plane into a
 // shared-memory pipeline S planes ahead of the compute:
 //
-//   cur ring  : 2R+S slots, each the (32*NX + 2R) x (TY + 2R) box of u(t) at
+//   cur ring  : 2R+S slots, each the (32*NX + 2RA) x (TY + 2R) box of u(t) at
 //               one a0 plane, halo included (TMA zero-fills out-of-range
 //               boxes at the grid faces, which only feed non-stored points);
 //               the a0 neighbours of plane z are the same (a1, a2) position
@@ -30,7 +30,7 @@
 namespace sfb {
 
 struct TmaStencilArgs {
-    CUtensorMap cur;   // box (WB, TY+2R, 1) at (x0-R, y0-R, z)
+    CUtensorMap cur;   // box (WB, TY+2R, 1) at (x0-RA, y0-R, z)
     CUtensorMap prev;  // box (32*NX, TY, 1)
     CUtensorMap m;     // box (32*NX, TY, 1)
     CUtensorMap eta;   // box (32*NX, TY, 1)
@@ -78,13 +78,18 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// The innermost box coordinate must be 16-byte aligned (measured: boxes
+// starting at x0 - R fault with an illegal instruction unless 4R is a
+// multiple of 16), so the a2 halo is widened to RA = R rounded up to 4.
 template <int R, int NX>
 struct TmaBox {
-    static constexpr int WB = (32 * NX + 2 * R + 3) / 4 * 4;  // 16-byte multiple rows
+    static constexpr int RA = (R + 3) / 4 * 4;
+    static constexpr int WB = 32 * NX + 2 * RA;  // 16-byte multiple rows
 };
 
 template <int R, int TY, int NX>
 struct TmaLayout {
+    static constexpr int RA = TmaBox<R, NX>::RA;
     static constexpr int WB = TmaBox<R, NX>::WB;
     static constexpr int H = TY + 2 * R;
     static constexpr int CUR_FLOATS = WB * H;
@@ -102,6 +107,7 @@ template <int R, bool FWD, int TY, int NX>
 __global__ void __launch_bounds__(32 * TY) acoustic3d_tma_kernel(const __grid_constant__ TmaStencilArgs A) {
     using L = TmaLayout<R, TY, NX>;
     constexpr int WB = L::WB;
+    constexpr int RA = L::RA;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     unsigned char* cur_base = smem + L::BAR_BYTES;
@@ -129,7 +135,7 @@ __global__ void __launch_bounds__(32 * TY) acoustic3d_tma_kernel(const __grid_co
         uint64_t* b = &bar[i % S];
         const int z = zb + i;
         mbar_arrive_expect_tx(b, group_bytes);
-        tma_load_3d(cur_slot(z + R), &A.cur, x0 - R, y0 - R, z + R, b);
+        tma_load_3d(cur_slot(z + R), &A.cur, x0 - RA, y0 - R, z + R, b);
         tma_load_3d(pme_slot(i, 0), &A.prev, x0, y0, z, b);
         tma_load_3d(pme_slot(i, 1), &A.m, x0, y0, z, b);
         tma_load_3d(pme_slot(i, 2), &A.eta, x0, y0, z, b);
@@ -145,7 +151,7 @@ __global__ void __launch_bounds__(32 * TY) acoustic3d_tma_kernel(const __grid_co
         // prologue: planes zb-R .. zb+R-1 of cur on the extra barrier
         mbar_arrive_expect_tx(&bar[S], 2 * R * L::CUR_FLOATS * 4);
         for (int j = 0; j < 2 * R; ++j)
-            tma_load_3d(cur_slot(zb - R + j), &A.cur, x0 - R, y0 - R, zb - R + j, &bar[S]);
+            tma_load_3d(cur_slot(zb - R + j), &A.cur, x0 - RA, y0 - R, zb - R + j, &bar[S]);
         for (int i = 0; i < S && i < nit; ++i) issue_group(i);
     }
 
@@ -156,7 +162,7 @@ __global__ void __launch_bounds__(32 * TY) acoustic3d_tma_kernel(const __grid_co
         const int a1 = y0 + ty;
         if (a2 >= R && a2 < A.n2 - R && a1 >= R && a1 < A.n1 - R) act |= 1u << k;
     }
-    const int cpos = (ty + R) * WB + tx + R;  // centre of column k=0 in a cur tile
+    const int cpos = (ty + R) * WB + tx + RA;  // centre of column k=0 in a cur tile
     const int ppos = ty * 32 * NX + tx;
     float* outp = A.out + static_cast<int64_t>(zb) * A.plane +
                   static_cast<int64_t>(y0 + ty) * A.pitch + x0 + tx;
