@@ -42,6 +42,8 @@ CONFIGS = {
     # SURVEY C3 / BASELINE configs[2] (one order per run)
     "c3o4": dict(shape=(512, 512, 512), order=4, nt=500, boundary=40, spacing=10.0,
                  random=True),
+    "c3o6": dict(shape=(512, 512, 512), order=6, nt=500, boundary=40, spacing=10.0,
+                 random=True),
     "c3o8": dict(shape=(512, 512, 512), order=8, nt=500, boundary=40, spacing=10.0,
                  random=True),
     "c3o12": dict(shape=(512, 512, 512), order=12, nt=500, boundary=40, spacing=10.0,

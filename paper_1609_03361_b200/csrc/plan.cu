@@ -394,8 +394,9 @@ void setup_tma(Plan& p) {
     }
     make_tensor_map(&p.tm_m, p, p.m, static_cast<uint32_t>(32 * nx), 8);
     make_tensor_map(&p.tm_eta, p, p.eta, static_cast<uint32_t>(32 * nx), 8);
-    // deepest pipeline that still lets 2 CTAs share an SM
-    int stages = 6;
+    // 3 planes in flight measured best on B200 (c2: S=3 86.6 us, S=4 101 us,
+    // S=8 161 us per launch: occupancy beats depth); at least 2 CTAs per SM
+    int stages = 3;
     while (stages > 2 && tma_smem_bytes(r, nx, stages) * 2 > 220 * 1024) --stages;
     if (const char* env = std::getenv("SF_TMA_STAGES")) {
         const int v = std::atoi(env);
@@ -787,10 +788,18 @@ void choose_geometry(Plan& p) {
 
 // Switch a 3D plan to the TMA pipeline once its slots exist (SF_NO_TMA=1
 // keeps the per-thread-load kernel, for comparisons).
+//
+// Used for radius <= 3 (space order <= 6), where the stencil is memory-bound
+// and the pipeline wins (c2 order 4: 86.6 us vs 111 us per launch). At
+// higher orders the kernel is issue-bound, the ring's 2R extra LDS per point
+// cost more than the register queue's moves (c3 order 16: 1578 vs 1027 us),
+// so the per-thread-load kernel stays (SF_TMA=1 forces the pipeline).
 void enable_tma(Plan& p) {
     if (p.ndim != 3) return;
     if (const char* env = std::getenv("SF_NO_TMA"))
         if (env[0] == '1') return;
+    const char* force = std::getenv("SF_TMA");
+    if (p.ac.radius > 3 && !(force && force[0] == '1')) return;
     if (p.ac.radius > 4 && !std::getenv("SF_TILE")) p.tile_nx = 1;
     setup_tma(p);
     p.use_tma = true;
