@@ -329,6 +329,45 @@ __global__ void __launch_bounds__(256) sample_kernel(const SampleArgs A) {
 }
 
 // ---------------------------------------------------------------------------
+// K4+K5 fused for small point sets (one CTA): injection into the distinct
+// target cells, a CTA barrier, then sampling — the reference's two
+// sequential `omp single` loops (golden acoustic_3d.c:43-59) in one launch.
+template <int NDIM>
+__global__ void __launch_bounds__(1024) inject_sample_kernel(const InjectArgs I, const SampleArgs S) {
+    for (int i = threadIdx.x; i < I.ncells; i += blockDim.x) {
+        const int64_t off = I.cell_off[i];
+        float v = I.field[off];
+        const float mv = __ldg(I.m + off);
+        for (int j = I.start[i]; j < I.start[i + 1]; ++j) {
+            const float d =
+                __fdiv_rn(__fmul_rn(__fmul_rn(I.scale, __ldg(I.row + I.cp[j])), I.cw[j]), mv);
+            v = __fadd_rn(d, v);
+        }
+        I.field[off] = v;
+    }
+    __syncthreads();  // orders the injected stores before the samples' loads (CTA scope)
+    constexpr int C = 1 << NDIM;
+    for (int p = threadIdx.x; p < S.np; p += blockDim.x) {
+        const int c0 = S.ci[p * NDIM + 0];
+        const int c1 = S.ci[p * NDIM + 1];
+        const int c2 = NDIM == 3 ? S.ci[p * NDIM + 2] : 0;
+        float acc = 0.0f;
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            int64_t off;
+            if (NDIM == 3)
+                off = static_cast<int64_t>(c0 + (k & 1)) * S.plane +
+                      static_cast<int64_t>(c1 + ((k >> 1) & 1)) * S.pitch + (c2 + ((k >> 2) & 1));
+            else
+                off = static_cast<int64_t>(c0 + (k & 1)) * S.pitch + (c1 + ((k >> 1) & 1));
+            const float term = __fmul_rn(S.w[p * C + k], S.field[off]);
+            acc = k == 0 ? term : __fadd_rn(acc, term);
+        }
+        S.out[p] = acc;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // FWI: the gradient term for time t = 1 after the adjoint sweep
 // (grad += u(1) * ((v(2) - 2 v(1)) + v(0)) * cm on the interior).
 __global__ void __launch_bounds__(256)

@@ -582,6 +582,59 @@ void launch_sample(const Plan& p, const PointSet& s, const float* field, int64_t
         sample_kernel<2><<<g, 256, 0, p.stream>>>(A);
 }
 
+int64_t launches_per_step_of(const Plan& p) {
+    if (p.kind == Plan::DIFFUSION) return 1;
+    const PointSet& inj = p.ac.forward ? p.src : p.rec;
+    const PointSet& smp = p.ac.forward ? p.rec : p.src;
+    return (inj.ncells <= kFusedSparseMax && smp.np <= kFusedSparseMax) ? 2 : 3;
+}
+
+// One step of the reference time loop. Step k maps to t = k (forward) or
+// t = nt - k (adjoint); slot aliases as in codegen.cpp:336-354.
+// Injection then sampling on `field`: one fused single-CTA launch when both
+// point sets are small, else the two grid-wide kernels.
+constexpr int kFusedSparseMax = 4096;
+
+void launch_inject_sample(const Plan& p, const PointSet& inj, const PointSet& smp, float* field,
+                          int64_t row) {
+    if (inj.ncells <= kFusedSparseMax && smp.np <= kFusedSparseMax) {
+        InjectArgs I{};
+        I.field = field;
+        I.m = p.m;
+        I.row = inj.series + row * inj.np;
+        I.cell_off = inj.cell_off;
+        I.start = inj.start;
+        I.cp = inj.cp;
+        I.cw = inj.cw;
+        I.scale = p.ac.src_scale;
+        I.ncells = inj.np ? inj.ncells : 0;
+        SampleArgs S{};
+        S.field = field;
+        S.ci = smp.ci;
+        S.w = smp.w;
+        S.out = smp.series + row * smp.np;
+        S.pitch = p.pitch;
+        S.plane = p.plane;
+        S.np = static_cast<int>(smp.np);
+        const int threads = static_cast<int>(
+            std::min<int64_t>(1024, std::max<int64_t>(32, (std::max<int64_t>(I.ncells, smp.np) + 31) / 32 * 32)));
+        if (p.ndim == 3)
+            inject_sample_kernel<3><<<1, threads, 0, p.stream>>>(I, S);
+        else
+            inject_sample_kernel<2><<<1, threads, 0, p.stream>>>(I, S);
+        return;
+    }
+    launch_inject(p, inj, field, row);
+    launch_sample(p, smp, field, row);
+}
+
+int64_t launches_per_step_of(const Plan& p) {
+    if (p.kind == Plan::DIFFUSION) return 1;
+    const PointSet& inj = p.ac.forward ? p.src : p.rec;
+    const PointSet& smp = p.ac.forward ? p.rec : p.src;
+    return (inj.ncells <= kFusedSparseMax && smp.np <= kFusedSparseMax) ? 2 : 3;
+}
+
 // One step of the reference time loop. Step k maps to t = k (forward) or
 // t = nt - k (adjoint); slot aliases as in codegen.cpp:336-354.
 void enqueue_acoustic_step(Plan& p, int64_t k, float* const* u, bool stencil_only = false) {
@@ -592,8 +645,7 @@ void enqueue_acoustic_step(Plan& p, int64_t k, float* const* u, bool stencil_onl
         float* out = u[(t + 1) % 3];
         launch_stencil(p, out, cur, prev);
         if (stencil_only) return;
-        launch_inject(p, p.src, out, t);
-        launch_sample(p, p.rec, out, t);
+        launch_inject_sample(p, p.src, p.rec, out, t);
     } else {
         const int64_t t = p.nt - k;
         float* out = u[(t + 2) % 3];
@@ -601,8 +653,7 @@ void enqueue_acoustic_step(Plan& p, int64_t k, float* const* u, bool stencil_onl
         float* prev = u[(t + 1) % 3];
         launch_stencil(p, out, cur, prev);
         if (stencil_only) return;
-        launch_inject(p, p.rec, out, t - 1);
-        launch_sample(p, p.src, out, t - 1);
+        launch_inject_sample(p, p.rec, p.src, out, t - 1);
     }
 }
 
@@ -630,8 +681,7 @@ void enqueue_fwi_forward(Plan& p) {
     for (int64_t t = 0; t < p.nt; ++t) {
         float* out = p.hist + (t + 2) * L;
         launch_stencil(p, out, p.hist + (t + 1) * L, p.hist + t * L);
-        launch_inject(p, p.src, out, t);
-        launch_sample(p, p.rec, out, t);
+        launch_inject_sample(p, p.src, p.rec, out, t);
     }
 }
 
@@ -648,8 +698,7 @@ void enqueue_fwi_adjoint(Plan& p) {
             launch_stencil(p, out, cur, prev, p.grad, p.hist + (t + 2) * L);
         else
             launch_stencil(p, out, cur, prev);
-        launch_inject(p, p.rec, out, t - 1);
-        launch_sample(p, p.src, out, t - 1);
+        launch_inject_sample(p, p.rec, p.src, out, t - 1);
     }
     if (p.nt >= 1) {  // term for time 1
         dim3 b(128);
@@ -887,7 +936,7 @@ void setup_acoustic(Plan& p, const sf_acoustic_desc* d, int device, bool fwi) {
     p.arg_bytes = {3 * fb, fb, fb, d->nt * d->n_src * 4, d->n_src * p.ndim * 4,
                    d->n_src * corners * 4, d->nt * d->n_rec * 4, d->n_rec * p.ndim * 4,
                    d->n_rec * corners * 4};
-    p.launches_per_step = 3;
+    p.launches_per_step = 3;  // recomputed by launches_per_step_of()
 }
 
 void upload_acoustic(Plan& p, void* const* a) {
@@ -1132,7 +1181,7 @@ int sf_plan_time(sf_plan* p, float* total_ms, float* stencil_ms, int64_t* launch
         float ms = 0;
         SF_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
         if (total_ms) *total_ms = ms;
-        if (launches) *launches = p->launches_per_step * p->nt;
+        if (launches) *launches = sfb::launches_per_step_of(*p) * p->nt;
         if (stencil_ms) {
             // same steps with only the stencil launches: their summed duration
             sfb::run_steps(*p, sfb::kStencilOnly, sfb::kStencilOnly);
