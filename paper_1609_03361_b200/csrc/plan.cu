@@ -582,15 +582,6 @@ void launch_sample(const Plan& p, const PointSet& s, const float* field, int64_t
         sample_kernel<2><<<g, 256, 0, p.stream>>>(A);
 }
 
-int64_t launches_per_step_of(const Plan& p) {
-    if (p.kind == Plan::DIFFUSION) return 1;
-    const PointSet& inj = p.ac.forward ? p.src : p.rec;
-    const PointSet& smp = p.ac.forward ? p.rec : p.src;
-    return (inj.ncells <= kFusedSparseMax && smp.np <= kFusedSparseMax) ? 2 : 3;
-}
-
-// One step of the reference time loop. Step k maps to t = k (forward) or
-// t = nt - k (adjoint); slot aliases as in codegen.cpp:336-354.
 // Injection then sampling on `field`: one fused single-CTA launch when both
 // point sets are small, else the two grid-wide kernels.
 constexpr int kFusedSparseMax = 4096;
