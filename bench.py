@@ -365,6 +365,95 @@ def run_b200_arm(args, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
+def run_b200_slabs(args, world, rank, local):
+    """N > 1: weak scaling over depth slabs. The global grid stacks one c2-sized
+    block per GPU along axis 0 ((281 N) x 281 x 281, same boundary, source and
+    receiver line at the top); rank g owns 281 planes and swaps r-deep halos
+    with its neighbours over NCCL inside every time step (sf_plan_attach_nccl)."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1609_03361_b200 as sf
+    from paper_1609_03361_b200 import _lib
+    from paper_1609_03361_b200.slab import SlabPartition, SlabRun, nccl_unique_id
+    base, _, _ = make_model(args.config)
+    if CONFIGS[args.config]["random"]:
+        raise SystemExit("multi-GPU bench uses the c2 layered workload")
+    r = base.space_order // 2
+    gshape = (base.shape[0] * world,) + tuple(base.shape[1:])
+    model = sf.AcousticModel(shape=gshape, boundary_width=base.boundary_width,
+                             spacing=base.spacing, nt=base.nt, dt=base.dt,
+                             space_order=base.space_order, f0=base.f0, v_top=base.v_top,
+                             v_bottom=base.v_bottom, src_coords=base.src_coords,
+                             rec_coords=base.rec_coords)
+    g = sf.Grid()
+    m, eta = sf.build_medium(g, model)
+    src_ci = np.array([sf.interpolation_weights(c, model.spacing, gshape)[0]
+                       for c in model.src_coords], np.int32)
+    src_w = np.array([sf.interpolation_weights(c, model.spacing, gshape)[1]
+                      for c in model.src_coords], np.float32)
+    rec_ci = np.array([sf.interpolation_weights(c, model.spacing, gshape)[0]
+                       for c in model.rec_coords], np.int32)
+    rec_w = np.array([sf.interpolation_weights(c, model.spacing, gshape)[1]
+                      for c in model.rec_coords], np.float32)
+    t0 = 1.0 / model.f0
+    ser = np.array([sf.ricker_wavelet(model.f0, t * model.dt, t0) for t in range(model.nt)],
+                   np.float32)[:, None]
+    rec = np.zeros((model.nt, len(rec_ci)), np.float32)
+    part = SlabPartition.split(gshape[0], r, world, rank)
+    slab = SlabRun(part, gshape, model.space_order, True, model.nt, model.dt, model.spacing,
+                   m.data, eta.data, ser, src_ci, src_w, rec, rec_ci, rec_w, device=local)
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    slab.attach_nccl(obj[0], world, rank)
+    for _ in range(args.warmup):
+        slab.run(0, model.nt)
+    barrier(world)
+    tot = C.c_float()
+    nl = C.c_int64()
+    with ClockSampler(local) as clocks:
+        total = 0.0
+        for _ in range(args.steps):
+            sf.api.check(_lib.lib.sf_plan_time(slab.plan, C.byref(tot), None, C.byref(nl)))
+            total += tot.value
+    barrier(world)
+    ms_per_step = max_over_ranks(world, total / args.steps)
+    pts = 1
+    for e in gshape:
+        pts *= e - 2 * r
+    value = pts * model.nt / (ms_per_step / 1e3) / 1e9
+    # e2e: upload host slices, run, download, every step
+    barrier(world)
+    t_e = time.perf_counter()
+    for _ in range(args.steps):
+        argv = (C.c_void_p * 9)(*[b.ctypes.data for b in slab.bufs])
+        sf.api.check(_lib.lib.sf_plan_invoke(slab.plan, argv, 9))
+    e2e_s = max_over_ranks(world, (time.perf_counter() - t_e) / args.steps)
+    h2d = sum(b.nbytes for b in slab.bufs)
+    d2h = slab.bufs[0].nbytes + slab.bufs[3].nbytes + slab.bufs[6].nbytes
+    if rank == 0:
+        line = {
+            "metric": "GPts/s (grid-point updates/sec)", "value": value, "unit": "GPts/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config} stacked along depth: "
+                                   f"{'x'.join(map(str, gshape))}, order {model.space_order}, "
+                                   f"{model.nt} steps, {world} depth slabs of "
+                                   f"{base.shape[0]} planes, NCCL halo exchange ({r} planes) "
+                                   "every step", "grid": list(gshape),
+                       "parallelism": f"slab{world}", "interior_points": pts},
+            "e2e": {"value": pts * model.nt / e2e_s / 1e9, "unit": "GPts/s",
+                    "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world},
+            "gpu_launches": int(nl.value * args.steps),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    slab.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -379,6 +468,8 @@ def main():
     try:
         if args.impl == "reference":
             run_reference_arm(args, world, rank)
+        elif world > 1:
+            run_b200_slabs(args, world, rank, local)
         else:
             run_b200_arm(args, world, rank, local)
     finally:

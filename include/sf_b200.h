@@ -158,6 +158,33 @@ int sf_build_medium(int ndim, const int64_t *shape, int boundary_width,
 int sf_acoustic_constants(int ndim, int space_order, int forward, double dt,
                           double spacing, float *out /* [15] */, int *time_sel /* [3] */);
 
+/* ---- depth-slab decomposition (multi-GPU) -----------------
+ * A slab plan owns global axis-0 planes [own_begin, own_end) of a grid with
+ * global_n0 planes (own_end - own_begin >= r = space_order/2) and stores the
+ * r-deep halos on each internal side: desc->shape[0] = local planes with
+ * plane0 = max(own_begin - r, 0) the global index of local plane 0 and
+ * plane0 + shape[0] = min(own_end + r, global_n0). Buffers passed to the
+ * plan are the matching local slices (halo planes included); sparse cell
+ * indices are local. The slab updates only owned interior planes, applies
+ * only the injection corners it owns, and after each step's injection swaps
+ * r planes of the new level with its neighbours before sampling, so the
+ * result is bitwise the single-domain run. */
+typedef struct {
+    int64_t global_n0;
+    int64_t plane0;
+    int64_t own_begin, own_end;
+} sf_slab_desc;
+
+int sf_acoustic_plan_create_slab(const sf_acoustic_desc *desc, const sf_slab_desc *slab,
+                                 int device, sf_plan **out);
+/* Steps [step_begin, step_end) of an in-process chain of adjacent slab plans
+ * (ordered by depth; one or several devices), halo copies device-to-device. */
+int sf_slab_chain_run(sf_plan *const *plans, int nplans, int64_t step_begin, int64_t step_end);
+/* One process per GPU: NCCL send/recv halo exchange inside every step of
+ * sf_plan_run / sf_plan_invoke. id = 128-byte ncclUniqueId from rank 0. */
+int sf_nccl_unique_id(void *out, int bytes);
+int sf_plan_attach_nccl(sf_plan *plan, const void *id, int nranks, int rank);
+
 /* Folded diffusion constants (exact rationals -> double -> f32). */
 int sf_diffusion_constants(int order, int64_t alpha_num, int64_t alpha_den, int64_t dx_num,
                            int64_t dx_den, float *c0, int *has_c0, float *cj /* [8] */);

@@ -36,6 +36,8 @@ EXPORTS = [
     "sf_fwi_plan_create", "sf_fwi_gradient", "sf_fwi_time",
     "sf_interpolation_weights", "sf_stable_dt", "sf_ricker", "sf_build_medium",
     "sf_acoustic_constants", "sf_diffusion_constants",
+    "sf_acoustic_plan_create_slab", "sf_slab_chain_run", "sf_nccl_unique_id",
+    "sf_plan_attach_nccl",
 ]
 
 
@@ -53,6 +55,11 @@ class DiffusionDesc(C.Structure):
         ("alpha_num", C.c_int64), ("alpha_den", C.c_int64),
         ("dx_num", C.c_int64), ("dx_den", C.c_int64),
     ]
+
+
+class SlabDesc(C.Structure):
+    _fields_ = [("global_n0", C.c_int64), ("plane0", C.c_int64), ("own_begin", C.c_int64),
+                ("own_end", C.c_int64)]
 
 
 _vp = C.c_void_p
@@ -97,6 +104,11 @@ def _bind(lib):
                                           _f32p, _i32p]
     lib.sf_diffusion_constants.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                            C.POINTER(C.c_float), C.POINTER(C.c_int), _f32p]
+    lib.sf_acoustic_plan_create_slab.argtypes = [C.POINTER(AcousticDesc), C.POINTER(SlabDesc),
+                                                 C.c_int, C.POINTER(_vp)]
+    lib.sf_slab_chain_run.argtypes = [C.POINTER(_vp), C.c_int, C.c_int64, C.c_int64]
+    lib.sf_nccl_unique_id.argtypes = [C.c_char_p, C.c_int]
+    lib.sf_plan_attach_nccl.argtypes = [_vp, C.c_char_p, C.c_int, C.c_int]
     return lib
 
 

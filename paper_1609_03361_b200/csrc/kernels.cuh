@@ -34,6 +34,7 @@ struct StencilArgs {
     int64_t plane;       // plane stride (elements, 3D)
     int n0, n1, n2;
     int zchunk;          // planes of axis 0 per block (3D)
+    int z0, z1;          // planes of axis 0 this launch updates (interior, or a slab's)
     float ce, cm;
     float tc[3];
     float c0;
@@ -96,8 +97,8 @@ acoustic3d_kernel(const StencilArgs A) {
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int x0 = blockIdx.x * 32 * NX;
     const int a1 = blockIdx.y * TY + ty;
-    const int zb = R + blockIdx.z * A.zchunk;
-    const int ze = min(zb + A.zchunk, A.n0 - R);
+    const int zb = A.z0 + blockIdx.z * A.zchunk;
+    const int ze = min(zb + A.zchunk, A.z1);
     if (zb >= ze) return;  // uniform per CTA
 
     const int pitch = static_cast<int>(A.pitch);
@@ -237,7 +238,7 @@ template <int R, bool FWD>
 __global__ void __launch_bounds__(256) acoustic2d_kernel(const StencilArgs A) {
     const int a1 = blockIdx.x * blockDim.x + threadIdx.x;
     const int a0 = blockIdx.y * blockDim.y + threadIdx.y;
-    if (a1 < R || a1 >= A.n1 - R || a0 < R || a0 >= A.n0 - R) return;
+    if (a1 < R || a1 >= A.n1 - R || a0 < A.z0 || a0 >= A.z1) return;
     const int64_t o = static_cast<int64_t>(a0) * A.pitch + a1;
     const float* c = A.cur + o;
     const float ev = __ldg(A.eta + o), mv = __ldg(A.m + o), pv = __ldg(A.prev + o), cv = __ldg(c);

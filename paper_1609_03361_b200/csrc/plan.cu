@@ -8,6 +8,7 @@
 // Here: plan create = build time (constants folded, buffers allocated in HBM),
 // apply = H2D, nt steps replayed from a cached CUDA graph, D2H.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -107,6 +108,7 @@ struct sf_plan {
     // launch geometry
     dim3 grid3;
     int zchunk = 0;
+    int z0 = 0, z1 = 0;  // axis-0 planes the stencil updates (local coordinates)
     int tile_nx = 1, tile_ty = 8;  // 3D stencil tile: (32*tile_nx) x tile_ty
     int resident = 0;              // CTAs per SM of the chosen stencil kernel
     // TMA pipeline path (3D forward/adjoint without the FWI gradient)
@@ -119,6 +121,15 @@ struct sf_plan {
     std::vector<int64_t> arg_bytes;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int64_t launches_per_step = 0;
+    // depth-slab decomposition; a whole grid is one slab
+    bool slab = false;
+    int64_t global_n0 = 0, plane0 = 0, own_begin = 0, own_end = 0;
+    int own_lo = 0, own_hi = 0;  // owned planes in local coordinates
+    bool has_lower = false, has_upper = false;
+    // NCCL transport (one process per GPU)
+    void* nccl_comm = nullptr;
+    int nccl_rank = -1, nccl_nranks = 0;
+    cudaEvent_t ev_copy = nullptr;  // in-process chain: halo copies issued
 
     ~sf_plan();
 };
@@ -218,6 +229,8 @@ void upload_points(Plan& p, PointSet& s, const float* series, const int* ci, con
         for (int k = 0; k < corners; ++k) {
             int32_t c[3];
             for (int d = 0; d < p.ndim; ++d) c[d] = s.host_ci[q * p.ndim + d] + ((k >> d) & 1);
+            // a slab applies only the corners it owns; neighbours apply theirs
+            if (c[0] < p.own_lo || c[0] >= p.own_hi) continue;
             cs.push_back({device_offset(p, c), static_cast<int>(q), w[q * corners + k]});
         }
     // stable sort by cell keeps ascending p within a cell
@@ -235,11 +248,17 @@ void upload_points(Plan& p, PointSet& s, const float* series, const int* ci, con
         cw.push_back(cs[i].w);
     }
     start.push_back(static_cast<int>(cs.size()));
+    if (cells.empty()) {  // nothing owned: keep a valid empty CSR
+        cells.push_back(0);
+        start.assign(2, 0);
+        cp.push_back(0);
+        cw.push_back(0.0f);
+    }
     dfree(s.cell_off);
     dfree(s.start);
     dfree(s.cp);
     dfree(s.cw);
-    s.ncells = static_cast<int>(cells.size());
+    s.ncells = cs.empty() ? 0 : static_cast<int>(cells.size());
     s.cell_off = dalloc<int64_t>(cells.size());
     s.start = dalloc<int>(start.size());
     s.cp = dalloc<int>(cp.size());
@@ -483,6 +502,8 @@ StencilArgs stencil_args(const Plan& p, float* out, const float* cur, const floa
     A.n1 = static_cast<int>(p.n[1]);
     A.n2 = static_cast<int>(p.ndim == 3 ? p.n[2] : 1);
     A.zchunk = p.zchunk;
+    A.z0 = p.z0;
+    A.z1 = p.z1;
     A.ce = p.ac.ce;
     A.cm = p.ac.cm;
     for (int k = 0; k < 3; ++k) A.tc[k] = p.ac.tc[k];
@@ -515,6 +536,8 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
             T.n1 = static_cast<int>(p.n[1]);
             T.n2 = static_cast<int>(p.n[2]);
             T.zchunk = p.zchunk;
+            T.z0 = p.z0;
+            T.z1 = p.z1;
             T.stages = p.tma_stages;
             T.ce = p.ac.ce;
             T.cm = p.ac.cm;
@@ -582,6 +605,79 @@ void launch_sample(const Plan& p, const PointSet& s, const float* field, int64_t
         sample_kernel<2><<<g, 256, 0, p.stream>>>(A);
 }
 
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded at run time (dlopen) so the library never pins an NCCL build
+// into processes that also load PyTorch's: the copy already mapped in the
+// process (RTLD_NOLOAD) is preferred, else the system libnccl.so.2.
+struct NcclId {
+    char internal[128];  // ncclUniqueId
+};
+struct NcclApi {
+    int (*GetUniqueId)(NcclId*) = nullptr;
+    int (*CommInitRank)(void**, int, NcclId, int) = nullptr;
+    int (*CommDestroy)(void*) = nullptr;
+    int (*GroupStart)() = nullptr;
+    int (*GroupEnd)() = nullptr;
+    int (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(int) = nullptr;
+};
+constexpr int kNcclFloat32 = 7;  // ncclFloat32 in nccl.h
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static bool loaded = false;
+    if (loaded) return api;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) throw Status(SF_ERR_CUDA, "libnccl.so.2 not found");
+    auto sym = [&](const char* n) {
+        void* f = dlsym(h, n);
+        if (!f) throw Status(SF_ERR_CUDA, std::string("NCCL symbol missing: ") + n);
+        return f;
+    };
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+    api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    loaded = true;
+    return api;
+}
+
+void nccl_check(int rc, const char* what) {
+    if (rc != 0)
+        throw Status(SF_ERR_CUDA, std::string(what) + ": " + nccl().GetErrorString(rc));
+}
+
+// Halo exchange of the level just written (after injection, so halos carry
+// injected values): my first r owned planes go down, my last r owned planes
+// go up; the neighbours' planes land in my r-deep halos. Planes are
+// contiguous (axis 0 is the slowest), one message per face.
+void launch_exchange_nccl(const Plan& p, float* f) {
+    const NcclApi& N = nccl();
+    const int r = p.ac.radius;
+    const size_t count = static_cast<size_t>(r) * static_cast<size_t>(p.plane);
+    nccl_check(N.GroupStart(), "ncclGroupStart");
+    if (p.has_lower) {
+        nccl_check(N.Send(f + static_cast<int64_t>(p.own_lo) * p.plane, count, kNcclFloat32,
+                          p.nccl_rank - 1, p.nccl_comm, p.stream), "ncclSend");
+        nccl_check(N.Recv(f + static_cast<int64_t>(p.own_lo - r) * p.plane, count, kNcclFloat32,
+                          p.nccl_rank - 1, p.nccl_comm, p.stream), "ncclRecv");
+    }
+    if (p.has_upper) {
+        nccl_check(N.Send(f + static_cast<int64_t>(p.own_hi - r) * p.plane, count, kNcclFloat32,
+                          p.nccl_rank + 1, p.nccl_comm, p.stream), "ncclSend");
+        nccl_check(N.Recv(f + static_cast<int64_t>(p.own_hi) * p.plane, count, kNcclFloat32,
+                          p.nccl_rank + 1, p.nccl_comm, p.stream), "ncclRecv");
+    }
+    nccl_check(N.GroupEnd(), "ncclGroupEnd");
+}
+
 // Injection then sampling on `field`: one fused single-CTA launch when both
 // point sets are small, else the two grid-wide kernels.
 constexpr int kFusedSparseMax = 4096;
@@ -621,6 +717,7 @@ void launch_inject_sample(const Plan& p, const PointSet& inj, const PointSet& sm
 
 int64_t launches_per_step_of(const Plan& p) {
     if (p.kind == Plan::DIFFUSION) return 1;
+    if (p.nccl_comm && (p.has_lower || p.has_upper)) return 3;
     const PointSet& inj = p.ac.forward ? p.src : p.rec;
     const PointSet& smp = p.ac.forward ? p.rec : p.src;
     return (inj.ncells <= kFusedSparseMax && smp.np <= kFusedSparseMax) ? 2 : 3;
@@ -628,23 +725,79 @@ int64_t launches_per_step_of(const Plan& p) {
 
 // One step of the reference time loop. Step k maps to t = k (forward) or
 // t = nt - k (adjoint); slot aliases as in codegen.cpp:336-354.
-void enqueue_acoustic_step(Plan& p, int64_t k, float* const* u, bool stencil_only = false) {
+struct StepSlots {
+    float* out;
+    float* cur;
+    float* prev;
+    int64_t row;  // sparse series row of this step
+};
+
+StepSlots step_slots(const Plan& p, int64_t k, float* const* u) {
     if (p.ac.forward) {
         const int64_t t = k;
-        float* prev = u[(t + 2) % 3];
-        float* cur = u[t % 3];
-        float* out = u[(t + 1) % 3];
-        launch_stencil(p, out, cur, prev);
-        if (stencil_only) return;
-        launch_inject_sample(p, p.src, p.rec, out, t);
-    } else {
-        const int64_t t = p.nt - k;
-        float* out = u[(t + 2) % 3];
-        float* cur = u[t % 3];
-        float* prev = u[(t + 1) % 3];
-        launch_stencil(p, out, cur, prev);
-        if (stencil_only) return;
-        launch_inject_sample(p, p.rec, p.src, out, t - 1);
+        return {u[(t + 1) % 3], u[t % 3], u[(t + 2) % 3], t};
+    }
+    const int64_t t = p.nt - k;
+    return {u[(t + 2) % 3], u[t % 3], u[(t + 1) % 3], t - 1};
+}
+
+void enqueue_acoustic_step(Plan& p, int64_t k, float* const* u, bool stencil_only = false) {
+    const StepSlots st = step_slots(p, k, u);
+    const PointSet& inj = p.ac.forward ? p.src : p.rec;
+    const PointSet& smp = p.ac.forward ? p.rec : p.src;
+    launch_stencil(p, st.out, st.cur, st.prev);
+    if (stencil_only) return;
+    if (p.nccl_comm && (p.has_lower || p.has_upper)) {
+        launch_inject(p, inj, st.out, st.row);
+        launch_exchange_nccl(p, st.out);
+        launch_sample(p, smp, st.out, st.row);
+        return;
+    }
+    launch_inject_sample(p, inj, smp, st.out, st.row);
+}
+
+// In-process chain of slab plans (one host thread; plans on one or several
+// devices): per step every slab runs stencil + injection, copies its
+// boundary planes into its neighbours' halos on its own stream, and samples
+// once the neighbours' copies into its halos are done. Ordering across
+// streams uses one event per plan (recorded after its copies).
+void chain_step(sf_plan* const* P, int n, int64_t k) {
+    const int r = P[0]->ac.radius;
+    for (int i = 0; i < n; ++i) {
+        Plan& p = *P[i];
+        SF_CUDA(cudaSetDevice(p.device));
+        if (k > 0) {  // neighbours' halo copies of the previous step landed
+            if (i > 0) SF_CUDA(cudaStreamWaitEvent(p.stream, P[i - 1]->ev_copy, 0));
+            if (i + 1 < n) SF_CUDA(cudaStreamWaitEvent(p.stream, P[i + 1]->ev_copy, 0));
+        }
+        const StepSlots st = step_slots(p, k, p.slot);
+        launch_stencil(p, st.out, st.cur, st.prev);
+        launch_inject(p, p.ac.forward ? p.src : p.rec, st.out, st.row);
+        const size_t bytes = static_cast<size_t>(r) * p.plane * sizeof(float);
+        if (i > 0) {
+            Plan& q = *P[i - 1];
+            const StepSlots sq = step_slots(q, k, q.slot);
+            SF_CUDA(cudaMemcpyPeerAsync(sq.out + static_cast<int64_t>(q.own_hi) * q.plane, q.device,
+                                        st.out + static_cast<int64_t>(p.own_lo) * p.plane,
+                                        p.device, bytes, p.stream));
+        }
+        if (i + 1 < n) {
+            Plan& q = *P[i + 1];
+            const StepSlots sq = step_slots(q, k, q.slot);
+            SF_CUDA(cudaMemcpyPeerAsync(sq.out + static_cast<int64_t>(q.own_lo - r) * q.plane,
+                                        q.device,
+                                        st.out + static_cast<int64_t>(p.own_hi - r) * p.plane,
+                                        p.device, bytes, p.stream));
+        }
+        SF_CUDA(cudaEventRecord(p.ev_copy, p.stream));
+    }
+    for (int i = 0; i < n; ++i) {
+        Plan& p = *P[i];
+        SF_CUDA(cudaSetDevice(p.device));
+        if (i > 0) SF_CUDA(cudaStreamWaitEvent(p.stream, P[i - 1]->ev_copy, 0));
+        if (i + 1 < n) SF_CUDA(cudaStreamWaitEvent(p.stream, P[i + 1]->ev_copy, 0));
+        const StepSlots st = step_slots(p, k, p.slot);
+        launch_sample(p, p.ac.forward ? p.rec : p.src, st.out, st.row);
     }
 }
 
@@ -763,7 +916,7 @@ void set_grid(Plan& p) {
     const int r = p.ac.radius;
     const int64_t wx = 32 * p.tile_nx;
     const int64_t gx = (p.n[2] + wx - 1) / wx, gy = (p.n[1] + p.tile_ty - 1) / p.tile_ty;
-    const int64_t nz = p.n[0] - 2 * r;
+    const int64_t nz = p.z1 - p.z0;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
     int per_sm = 0;
@@ -915,6 +1068,13 @@ void setup_acoustic(Plan& p, const sf_acoustic_desc* d, int device, bool fwi) {
     p.nt = d->nt;
     p.ac = acoustic_constants(d->ndim, d->space_order, fwi ? true : d->forward != 0, d->dt,
                               d->spacing);
+    p.z0 = p.ac.radius;
+    p.z1 = static_cast<int>(p.n[0]) - p.ac.radius;
+    p.global_n0 = p.n[0];
+    p.own_begin = 0;
+    p.own_end = p.n[0];
+    p.own_lo = 0;
+    p.own_hi = static_cast<int>(p.n[0]);
     p.m = alloc_field(p);
     p.eta = alloc_field(p);
     alloc_points(p, p.src, d->n_src, d->nt);
@@ -1027,6 +1187,13 @@ sf_plan::~sf_plan() {
     for (float* s : v) sfb::dfree(s);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (ev_copy) cudaEventDestroy(ev_copy);
+    if (nccl_comm) {
+        try {
+            sfb::nccl().CommDestroy(nccl_comm);
+        } catch (...) {
+        }
+    }
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -1088,6 +1255,89 @@ int sf_diffusion_plan_create(const sf_diffusion_desc* d, int device, sf_plan** o
 }
 
 void sf_plan_destroy(sf_plan* p) { delete p; }
+
+int sf_acoustic_plan_create_slab(const sf_acoustic_desc* d, const sf_slab_desc* sl, int device,
+                                 sf_plan** out) {
+    if (!out || !d || !sl) return SF_ERR_INVALID;
+    *out = nullptr;
+    auto p = std::make_unique<sf_plan>();
+    p->kind = sf_plan::ACOUSTIC;
+    int rc = guard([&] {
+        if (d->ndim != 3) throw Status(SF_ERR_INVALID, "slab decomposition is 3D");
+        const int64_t r = d->space_order / 2;
+        const int64_t n0 = d->shape[0];
+        if (sl->own_begin < 0 || sl->own_end > sl->global_n0 || sl->own_end - sl->own_begin < r ||
+            sl->plane0 != std::max<int64_t>(sl->own_begin - r, 0) ||
+            sl->plane0 + n0 != std::min<int64_t>(sl->own_end + r, sl->global_n0))
+            throw Status(SF_ERR_INVALID,
+                         "slab: shape[0] must be the owned planes plus r-deep halos, owned >= r");
+        sfb::setup_acoustic(*p, d, device, false);
+        for (int s = 0; s < 3; ++s) p->slot[s] = sfb::alloc_field(*p);
+        p->slab = true;
+        p->global_n0 = sl->global_n0;
+        p->plane0 = sl->plane0;
+        p->own_begin = sl->own_begin;
+        p->own_end = sl->own_end;
+        p->own_lo = static_cast<int>(sl->own_begin - sl->plane0);
+        p->own_hi = static_cast<int>(sl->own_end - sl->plane0);
+        p->has_lower = sl->own_begin > 0;
+        p->has_upper = sl->own_end < sl->global_n0;
+        p->z0 = static_cast<int>(std::max<int64_t>(sl->own_begin, r) - sl->plane0);
+        p->z1 = static_cast<int>(std::min<int64_t>(sl->own_end, sl->global_n0 - r) - sl->plane0);
+        SF_CUDA(cudaEventCreateWithFlags(&p->ev_copy, cudaEventDisableTiming));
+        sfb::choose_geometry(*p);
+        sfb::enable_tma(*p);
+        SF_CUDA(cudaStreamSynchronize(p->stream));
+    });
+    if (rc == SF_OK) *out = p.release();
+    return rc;
+}
+
+int sf_slab_chain_run(sf_plan* const* plans, int nplans, int64_t b, int64_t e) {
+    return guard([&] {
+        if (!plans || nplans < 1) throw Status(SF_ERR_INVALID, "no plans");
+        for (int i = 0; i < nplans; ++i) {
+            const sf_plan* p = plans[i];
+            if (!p || !p->slab || p->kind != sf_plan::ACOUSTIC)
+                throw Status(SF_ERR_INVALID, "chain needs acoustic slab plans");
+            if (p->nt != plans[0]->nt || p->ac.radius != plans[0]->ac.radius ||
+                p->plane != plans[0]->plane || p->ac.forward != plans[0]->ac.forward)
+                throw Status(SF_ERR_INVALID, "chain plans disagree");
+            if (i > 0 && plans[i - 1]->own_end != p->own_begin)
+                throw Status(SF_ERR_INVALID, "chain slabs must be adjacent and ordered");
+        }
+        if (b < 0 || e > plans[0]->nt || b > e) throw Status(SF_ERR_INVALID, "step range");
+        for (int64_t k = b; k < e; ++k) sfb::chain_step(plans, nplans, k);
+        for (int i = 0; i < nplans; ++i) sfb::check_kernel_errors(*plans[i]);
+    });
+}
+
+int sf_nccl_unique_id(void* out, int bytes) {
+    return guard([&] {
+        if (bytes < 128) throw Status(SF_ERR_INVALID, "need 128 bytes");
+        sfb::NcclId id;
+        sfb::nccl_check(sfb::nccl().GetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(out, id.internal, 128);
+    });
+}
+
+int sf_plan_attach_nccl(sf_plan* p, const void* id, int nranks, int rank) {
+    if (!p) return SF_ERR_INVALID;
+    return guard([&] {
+        if (!p->slab) throw Status(SF_ERR_INVALID, "NCCL exchange needs a slab plan");
+        if (rank < 0 || rank >= nranks) throw Status(SF_ERR_INVALID, "rank out of range");
+        SF_CUDA(cudaSetDevice(p->device));
+        sfb::NcclId nid;
+        std::memcpy(nid.internal, id, 128);
+        void* comm = nullptr;
+        sfb::nccl_check(sfb::nccl().CommInitRank(&comm, nranks, nid, rank), "ncclCommInitRank");
+        p->nccl_comm = comm;
+        p->nccl_rank = rank;
+        p->nccl_nranks = nranks;
+        for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+        p->graphs.clear();
+    });
+}
 
 int sf_plan_num_args(const sf_plan* p) { return p ? static_cast<int>(p->arg_names.size()) : 0; }
 

@@ -38,6 +38,7 @@ struct TmaStencilArgs {
     int pitch, plane;  // elements
     int n0, n1, n2;
     int zchunk;
+    int z0, z1;  // planes of axis 0 this launch updates
     int stages;
     float ce, cm;
     float tc[3];
@@ -119,8 +120,8 @@ __global__ void __launch_bounds__(32 * TY) acoustic3d_tma_kernel(const __grid_co
     const int tid = ty * 32 + tx;
     const int x0 = blockIdx.x * 32 * NX;
     const int y0 = blockIdx.y * TY;
-    const int zb = R + blockIdx.z * A.zchunk;
-    const int ze = min(zb + A.zchunk, A.n0 - R);
+    const int zb = A.z0 + blockIdx.z * A.zchunk;
+    const int ze = min(zb + A.zchunk, A.z1);
     if (zb >= ze) return;  // uniform per CTA
     const int nit = ze - zb;
 
