@@ -36,6 +36,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
+    # SURVEY C1 / BASELINE configs[0]: 2D diffusion, exact 1/4 weights
+    "c1": dict(kind="diffusion", n=2048, nt=500, order=2),
+    # SURVEY C4 at one GPU: the 1024^3 per-GPU slab, order 8, 8 sources
+    "c4": dict(shape=(1024, 1024, 1024), order=8, nt=1000, boundary=40, spacing=10.0,
+               random=True, smooth="sines", nsrc=8),
+    # FWI gradient, forward with full history + adjoint/gradient
+    "c5": dict(kind="fwi", shape=(301, 301, 301), order=8, nt=1000, boundary=40, spacing=10.0),
     # SURVEY C2 / BASELINE configs[1]
     "c2": dict(shape=(281, 281, 281), order=4, nt=625, boundary=40, spacing=10.0,
                v_top=1500.0, v_bottom=2500.0, random=False),
@@ -74,6 +81,28 @@ def smooth_velocity(shape, seed, sigma=8.0, vmin=1500.0, vmax=4500.0):
     return vmin + (vmax - vmin) * (f.astype(np.float64) - lo) / (hi - lo)
 
 
+def smooth_velocity_sines(shape, seed, vmin=1500.0, vmax=4500.0, modes=6):
+    """Cheap smooth random velocity for very large grids (C4): a seeded sum
+    of separable sinusoids with wavelengths >= 40 cells, rescaled to
+    [vmin, vmax]. Built per plane (float64 only for one plane at a time)."""
+    rng = np.random.default_rng(seed)
+    n0, n1, n2 = shape
+    k = rng.uniform(2 * np.pi / 200, 2 * np.pi / 40, (modes, 3))
+    ph = rng.uniform(0, 2 * np.pi, (modes, 3))
+    amp = rng.uniform(0.5, 1.0, modes)
+    f1 = [np.cos(k[i, 1] * np.arange(n1) + ph[i, 1]) for i in range(modes)]
+    f2 = [np.cos(k[i, 2] * np.arange(n2) + ph[i, 2]) for i in range(modes)]
+    f0 = [np.cos(k[i, 0] * np.arange(n0) + ph[i, 0]) for i in range(modes)]
+    tot = float(amp.sum())
+    v = np.empty(shape, np.float64)
+    for a in range(n0):
+        pl = np.zeros((n1, n2))
+        for i in range(modes):
+            pl += amp[i] * f0[i][a] * np.outer(f1[i], f2[i])
+        v[a] = vmin + (vmax - vmin) * (pl / tot + 1.0) * 0.5
+    return v
+
+
 def make_model(cfg_name):
     import paper_1609_03361_b200 as sf
     c = CONFIGS[cfg_name]
@@ -93,6 +122,13 @@ def make_model(cfg_name):
                              space_order=c["order"], f0=10.0, v_top=4500.0, v_bottom=4500.0)
     model.dt = min(0.4 * h / 4500.0, model.stable_dt())
     mid = shape[1] // 2
+    if c.get("nsrc", 1) > 1:  # C4: seeded random interior source positions
+        rng = np.random.default_rng(8)
+        r = c["order"] // 2
+        model.src_coords = [[rng.uniform(bw + r, e - bw - r - 1) * h for e in shape]
+                            for _ in range(c["nsrc"])]
+        model.rec_coords = [[(bw + 10) * h, (bw + 2 + 7.3 * i) * h, mid * h] for i in range(101)]
+        return model, smooth_velocity_sines(shape, 1234), 1500.0
     model.src_coords = [[(bw + 2) * h, mid * h, mid * h]]
     lo, hi = (bw + 2) * h, (shape[1] - bw - 3) * h
     g = np.linspace(lo + 0.37 * h, hi - 0.41 * h, 256)
@@ -254,6 +290,23 @@ def cpu_reference_sample(model, cfg_name, v_field, v_min, steps=1, warmup=1, bud
 def run_reference_arm(args, world, rank):
     if rank != 0:
         return
+    if CONFIGS[args.config].get("kind") == "diffusion":
+        c = CONFIGS[args.config]
+        base = cpu_diffusion_sample(c["n"], c["nt"], args.cpu_budget)
+        print(json.dumps({"impl": "reference", "metric": "GPts/s (grid-point updates/sec)",
+                          "value": base["value"], "unit": "GPts/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+                          "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                          "data": "synthetic", "config": {"workload": args.config},
+                          "cpu_baseline": base,
+                          "e2e": {"value": base["value"], "unit": "GPts/s",
+                                  "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+              flush=True)
+        return
+    if CONFIGS[args.config].get("kind") == "fwi":
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "the reference has no FWI gradient (SPEC.md:635,639)"}), flush=True)
+        return
     model, v, vmin = make_model(args.config)
     base = cpu_reference_sample(model, args.config, v, vmin, steps=args.steps,
                                 warmup=args.warmup, budget_s=args.cpu_budget)
@@ -365,6 +418,170 @@ def run_b200_arm(args, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
+def run_b200_diffusion(args, world, rank, local):
+    """C1: 2048^2 diffusion, alpha 1/2, dx 1/2047, dt = dx^2/4 (weights exactly
+    1/4), 500 steps, seeded U[0,1) interior. 2 x 16 MiB slots: L2-resident."""
+    from fractions import Fraction
+
+    import paper_1609_03361_b200 as sf
+    c = CONFIGS[args.config]
+    n, nt = c["n"], c["nt"]
+    cfg = sf.DiffusionConfig(nx=n, ny=n, alpha=Fraction(1, 2), dx=Fraction(1, n - 1),
+                             dy=Fraction(1, n - 1), nt=nt, order=c["order"])
+    b = sf.make_diffusion_operator(cfg, device=local, pinned=True)
+    rng = np.random.default_rng(2016)
+    u0 = np.zeros((n, n), np.float32)
+    u0[1:-1, 1:-1] = rng.random((n - 2, n - 2))
+    b.u.data[0] = u0
+    b.u.data[1] = u0
+    op = b.op
+    op.upload()
+    for _ in range(args.warmup):
+        op.run(0, nt)
+    op.synchronize()
+    pts = (n - 2) ** 2
+    with ClockSampler(local) as clocks:
+        total = 0.0
+        for _ in range(args.steps):
+            t, _, nl = op.time(stencil=False)
+            total += t
+    ms = total / args.steps
+    value = pts * nt / (ms / 1e3) / 1e9
+    launch_ms = ms / nt
+    peak, peak_kind = load_peaks()
+    achieved = 8 * pts / (launch_ms / 1e3) / 1e9
+    op.apply()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        b.u.data[0] = u0
+        b.u.data[1] = u0
+        op.apply()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    base = None
+    if not args.no_cpu_baseline:
+        base = cpu_diffusion_sample(n, nt, args.cpu_budget)
+    line = {
+        "metric": "GPts/s (grid-point updates/sec)", "value": value, "unit": "GPts/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"c1: 2D diffusion {n}^2, order 2, {nt} steps, alpha 1/2, "
+                               f"dx 1/{n - 1}, dt = dx^2/4", "interior_points": pts,
+                   "l2": "2 x 16 MiB slots are L2-resident (126 MB L2); HBM roofline is "
+                         "a lower bound here"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                     "kernel": f"diffusion_kernel<R=1> avg launch {launch_ms * 1e3:.2f} us",
+                     "alg_bytes_per_launch": 8 * pts},
+        "cpu_baseline": base,
+        "e2e": {"value": pts * nt / e2e_s / 1e9, "unit": "GPts/s",
+                "h2d_bytes_per_step": b.u.data.nbytes, "d2h_bytes_per_step": b.u.data.nbytes},
+        "gpu_launches": int(nl * args.steps), "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_diffusion_sample(n, nt, budget_s):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as ol
+    rng = np.random.default_rng(2016)
+    u0 = np.zeros((n, n), np.float32)
+    u0[1:-1, 1:-1] = rng.random((n - 2, n - 2))
+    if ol.have_ref():
+        ref = ol.Ref()
+        ref.set_threads(ref.max_threads())
+        def timed(k):
+            op = ol.ref_diffusion(ref, n, n, (1, 2), (1, n - 1), k, 2)
+            op.set("u", np.stack([u0, u0]))
+            op.build()
+            t = time.perf_counter()
+            op.apply()
+            return time.perf_counter() - t
+        cal = timed(10)
+        k = int(max(10, min(nt, budget_s / max(cal / 10, 1e-6))))
+        secs = timed(k)
+        kind, cores = "reference", ref.max_threads()
+    else:
+        port = ol.Port()
+        import multiprocessing
+        k = 20
+        u = np.stack([u0, u0])
+        t = time.perf_counter()
+        port.diffusion_run(u, 2, (1, 2), (1, n - 1), k)
+        secs = time.perf_counter() - t
+        kind, cores = "port", multiprocessing.cpu_count()
+    return {"value": (n - 2) ** 2 * k / secs / 1e9, "unit": "GPts/s", "cores": cores,
+            "kind": kind, "sample": f"c1 {n}^2 diffusion, {k} of {nt} steps, JIT excluded"}
+
+
+def run_b200_fwi(args, world, rank, local):
+    """C5: forward with the full wavefield history in HBM (nt+2 levels of
+    301^3), adjoint injecting seeded N(0,1) residuals at 201 x 201 surface
+    receivers, gradient accumulated in the adjoint stencil. The metric counts
+    the updates of both passes."""
+    import paper_1609_03361_b200 as sf
+    c = CONFIGS[args.config]
+    shape, order, nt, bw, h = c["shape"], c["order"], c["nt"], c["boundary"], c["spacing"]
+    r = order // 2
+    v = smooth_velocity(shape, 1234)
+    g = sf.Grid()
+    model = sf.AcousticModel(shape=shape, boundary_width=bw, spacing=h, nt=nt,
+                             space_order=order, v_top=4500.0, v_bottom=4500.0)
+    dt = min(0.4 * h / 4500.0, model.stable_dt())
+    m, eta = sf.build_medium(g, model, v_field=v, v_min=1500.0)
+    mid = shape[1] // 2
+    src_c = [[(bw + 2) * h, mid * h, mid * h]]
+    rec_c = [[(bw + 10) * h, (bw + i) * h, (bw + j) * h] for i in range(201) for j in range(201)]
+    def interp(coords):
+        cis, ws = zip(*[sf.interpolation_weights(cc, h, shape) for cc in coords])
+        return np.array(cis, np.int32), np.array(ws, np.float32)
+    src_ci, src_w = interp(src_c)
+    rec_ci, rec_w = interp(rec_c)
+    t0 = 1.0 / 10.0
+    src = np.array([sf.ricker_wavelet(10.0, t * dt, t0) for t in range(nt)], np.float32)[:, None]
+    rng = np.random.default_rng(5)
+    residual = rng.standard_normal((nt, len(rec_c)), dtype=np.float32)
+    plan = sf.FwiPlan(shape, order, nt, dt, h, 1, len(rec_c), device=local)
+    t_e = time.perf_counter()
+    rec_out, grad, _, _ = plan.gradient(m.data, eta.data, src, src_ci, src_w, rec_ci, rec_w,
+                                        residual)
+    e2e_s = time.perf_counter() - t_e
+    fwd = adj = 0.0
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            f, a = plan.time()
+            fwd += f
+            adj += a
+    fwd /= args.steps
+    adj /= args.steps
+    pts = 1
+    for e in shape:
+        pts *= e - 2 * r
+    value = 2 * pts * nt / ((fwd + adj) / 1e3) / 1e9
+    peak, peak_kind = load_peaks()
+    line = {
+        "metric": "GPts/s (grid-point updates/sec)", "value": value, "unit": "GPts/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": 1, "ms_per_step": fwd + adj,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"c5: FWI gradient {shape[0]}^3, order {order}, {nt} steps, "
+                               f"history {nt + 2} levels in HBM, {len(rec_c)} receivers",
+                   "forward_ms": fwd, "adjoint_gradient_ms": adj,
+                   "grad_abs_max": float(np.abs(grad).max())},
+        "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_kind,
+                     "forward_achieved": 20 * pts * nt / (fwd / 1e3) / 1e9,
+                     "adjoint_achieved": 36 * pts * nt / (adj / 1e3) / 1e9,
+                     "achieved": (20 + 36) * pts * nt / ((fwd + adj) / 1e3) / 1e9,
+                     "frac": (20 + 36) * pts * nt / ((fwd + adj) / 1e3) / 1e9 / peak,
+                     "traffic": None},
+        "e2e": {"value": 2 * pts * nt / e2e_s / 1e9, "unit": "GPts/s",
+                "h2d_bytes_per_step": m.data.nbytes * 2 + residual.nbytes + src.nbytes,
+                "d2h_bytes_per_step": grad.nbytes + rec_out.nbytes},
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_b200_slabs(args, world, rank, local):
     """N > 1: weak scaling over depth slabs. The global grid stacks one c2-sized
     block per GPU along axis 0 ((281 N) x 281 x 281, same boundary, source and
@@ -466,8 +683,15 @@ def main():
     args = ap.parse_args()
     world, rank, local = dist_init(args)
     try:
+        kind = CONFIGS[args.config].get("kind", "acoustic")
         if args.impl == "reference":
             run_reference_arm(args, world, rank)
+        elif kind == "diffusion":
+            if rank == 0:
+                run_b200_diffusion(args, world, rank, local)
+        elif kind == "fwi":
+            if rank == 0:
+                run_b200_fwi(args, world, rank, local)
         elif world > 1:
             run_b200_slabs(args, world, rank, local)
         else:

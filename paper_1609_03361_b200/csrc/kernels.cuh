@@ -369,6 +369,20 @@ __global__ void __launch_bounds__(1024) inject_sample_kernel(const InjectArgs I,
 }
 
 // ---------------------------------------------------------------------------
+// Host-boundary repack between the reference's dense rows (width floats) and
+// the padded HBM rows (pitch floats): the H2D/D2H copies themselves are then
+// single contiguous transfers at full PCIe speed.
+__global__ void __launch_bounds__(256)
+repack_rows_kernel(float* __restrict__ dst, int64_t dst_pitch, const float* __restrict__ src,
+                   int64_t src_pitch, int64_t rows, int width) {
+    for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+        const float* s = src + row * src_pitch;
+        float* d = dst + row * dst_pitch;
+        for (int c = threadIdx.x; c < width; c += blockDim.x) d[c] = s[c];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // FWI: the gradient term for time t = 1 after the adjoint sweep
 // (grad += u(1) * ((v(2) - 2 v(1)) + v(0)) * cm on the interior).
 __global__ void __launch_bounds__(256)

@@ -98,6 +98,7 @@ struct sf_plan {
     sfb::DiffusionConstants dc{};
     // device mirrors
     float* slot[3] = {nullptr, nullptr, nullptr};
+    float* staging = nullptr;  // dense copy of one field for host transfers
     float* m = nullptr;
     float* eta = nullptr;
     sfb::PointSet src, rec;
@@ -148,18 +149,29 @@ int64_t field_numel(const Plan& p) {
 // rows of the dense reference layout (product of all but the last axis)
 int64_t dense_rows(const Plan& p) { return field_numel(p) / p.n[p.ndim - 1]; }
 
+// Dense host rows <-> padded device rows through a dense device staging
+// buffer: one contiguous copy (full PCIe rate) plus a repack kernel, instead
+// of a strided 2D copy of 1124-byte rows.
+unsigned repack_grid(int64_t rows) {
+    return static_cast<unsigned>(std::min<int64_t>(rows, 148 * 16));
+}
+
 void h2d_field(const Plan& p, float* dst, const float* src) {
     const int64_t last = p.n[p.ndim - 1];
-    SF_CUDA(cudaMemcpy2DAsync(dst, p.pitch * sizeof(float), src, last * sizeof(float),
-                              last * sizeof(float), dense_rows(p), cudaMemcpyHostToDevice,
-                              p.stream));
+    const int64_t rows = dense_rows(p);
+    SF_CUDA(cudaMemcpyAsync(p.staging, src, sizeof(float) * rows * last, cudaMemcpyHostToDevice,
+                            p.stream));
+    repack_rows_kernel<<<repack_grid(rows), 256, 0, p.stream>>>(dst, p.pitch, p.staging, last, rows,
+                                                               static_cast<int>(last));
 }
 
 void d2h_field(const Plan& p, float* dst, const float* src) {
     const int64_t last = p.n[p.ndim - 1];
-    SF_CUDA(cudaMemcpy2DAsync(dst, last * sizeof(float), src, p.pitch * sizeof(float),
-                              last * sizeof(float), dense_rows(p), cudaMemcpyDeviceToHost,
-                              p.stream));
+    const int64_t rows = dense_rows(p);
+    repack_rows_kernel<<<repack_grid(rows), 256, 0, p.stream>>>(p.staging, last, src, p.pitch, rows,
+                                                               static_cast<int>(last));
+    SF_CUDA(cudaMemcpyAsync(dst, p.staging, sizeof(float) * rows * last, cudaMemcpyDeviceToHost,
+                            p.stream));
 }
 
 int64_t device_offset(const Plan& p, const int32_t* c) {
@@ -1017,6 +1029,8 @@ void init_device(Plan& p, int device) {
     SF_CUDA(cudaEventCreate(&p.ev1));
 }
 
+int64_t field_slack(const Plan& p);
+
 void layout(Plan& p, int ndim, const int64_t* shape) {
     p.ndim = ndim;
     for (int i = 0; i < 3; ++i) p.n[i] = i < ndim ? shape[i] : 1;
@@ -1031,6 +1045,9 @@ void layout(Plan& p, int ndim, const int64_t* shape) {
     }
     for (int i = 0; i < ndim; ++i)
         if (shape[i] > (int64_t{1} << 30)) throw Status(SF_ERR_INVALID, "extent too large");
+    if (p.slot_elems + field_slack(p) >= (int64_t{1} << 31))
+        throw Status(SF_ERR_INVALID, "field exceeds 2^31 elements (32-bit offsets)");
+    p.staging = dalloc<float>(static_cast<size_t>(field_numel(p)));
 }
 
 // Guard slack after every field: the 3D stencil's tile loads are
@@ -1178,6 +1195,7 @@ sf_plan::~sf_plan() {
     if (stream) cudaStreamSynchronize(stream);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (float* s : slot) sfb::dfree(s);
+    sfb::dfree(staging);
     sfb::dfree(m);
     sfb::dfree(eta);
     sfb::free_points(src);
