@@ -27,6 +27,7 @@
 
 #include "kernels.cuh"
 #include "tma_stencil.cuh"
+#include "vec_stencil.cuh"
 #include "sf_internal.h"
 
 namespace sfb {
@@ -114,6 +115,8 @@ struct sf_plan {
     int resident = 0;              // CTAs per SM of the chosen stencil kernel
     // TMA pipeline path (3D forward/adjoint without the FWI gradient)
     bool use_tma = false;
+    bool use_vec = false;  // 4 points/thread, LDS.128 variant of the TMA pipeline
+    int vec_warps = 8;
     int tma_stages = 4;
     size_t tma_smem = 0;
     CUtensorMap tm_cur[3], tm_pme[3], tm_m, tm_eta;
@@ -384,6 +387,45 @@ size_t tma_smem_bytes(int r, int nx, int stages) {
     return 256 + static_cast<size_t>(2 * r + stages) * cur + static_cast<size_t>(stages) * 3 * pme;
 }
 
+// ---- vectorised TMA path (4 consecutive a2 points per thread) -------------
+template <bool FWD>
+const void* vec_ptr(int r, int warps) {
+#define SF_V(RR)                                                                              \
+    case RR:                                                                                  \
+        return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4>) \
+                          : reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 8>);
+    switch (r) {
+        SF_V(1) SF_V(2) SF_V(3) SF_V(4)
+        default: return nullptr;
+    }
+#undef SF_V
+}
+
+size_t vec_smem_bytes(int r, int warps, int stages) {
+    const int ra = (r + 3) / 4 * 4;
+    const int wb = 64 + 2 * ra, h = 2 * warps + 2 * r;
+    const int cur = (wb * h * 4 + 127) / 128 * 128;
+    const int pme = (64 * 2 * warps * 4 + 127) / 128 * 128;
+    return 256 + static_cast<size_t>(2 * r + stages) * cur + static_cast<size_t>(stages) * 3 * pme;
+}
+
+template <bool FWD>
+void launch_vec(int r, int warps, dim3 g, size_t smem, cudaStream_t st, const TmaStencilArgs& A) {
+    const dim3 b(32 * warps);
+#define SF_V(RR)                                                                   \
+    case RR:                                                                       \
+        if (warps == 4)                                                            \
+            acoustic3d_vec_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);              \
+        else                                                                       \
+            acoustic3d_vec_kernel<RR, FWD, 8><<<g, b, smem, st>>>(A);              \
+        return;
+    switch (r) {
+        SF_V(1) SF_V(2) SF_V(3) SF_V(4)
+        default: throw Status(SF_ERR_INVALID, "vector stencil compiled for radius <= 4");
+    }
+#undef SF_V
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -418,13 +460,33 @@ void make_tensor_map(CUtensorMap* map, const Plan& p, const float* base, uint32_
 void setup_tma(Plan& p) {
     const int r = p.ac.radius;
     const int nx = p.tile_nx;
-    const uint32_t wb = static_cast<uint32_t>(tma_box_width(r, nx));
+    const uint32_t wb = static_cast<uint32_t>(p.use_vec ? 64 + 2 * ((r + 3) / 4 * 4)
+                                                        : tma_box_width(r, nx));
+    const uint32_t ty = static_cast<uint32_t>(p.use_vec ? 2 * p.vec_warps : 8);
+    const uint32_t tx = static_cast<uint32_t>(p.use_vec ? 64 : 32 * nx);
     for (int s = 0; s < 3; ++s) {
-        make_tensor_map(&p.tm_cur[s], p, p.slot[s], wb, static_cast<uint32_t>(8 + 2 * r));
-        make_tensor_map(&p.tm_pme[s], p, p.slot[s], static_cast<uint32_t>(32 * nx), 8);
+        make_tensor_map(&p.tm_cur[s], p, p.slot[s], wb, ty + static_cast<uint32_t>(2 * r));
+        make_tensor_map(&p.tm_pme[s], p, p.slot[s], tx, ty);
     }
-    make_tensor_map(&p.tm_m, p, p.m, static_cast<uint32_t>(32 * nx), 8);
-    make_tensor_map(&p.tm_eta, p, p.eta, static_cast<uint32_t>(32 * nx), 8);
+    make_tensor_map(&p.tm_m, p, p.m, tx, ty);
+    make_tensor_map(&p.tm_eta, p, p.eta, tx, ty);
+    if (p.use_vec) {
+        int stages = 3;
+        while (stages > 2 && vec_smem_bytes(r, p.vec_warps, stages) * 2 > 226 * 1024) --stages;
+        if (const char* env = std::getenv("SF_TMA_STAGES")) {
+            const int v = std::atoi(env);
+            if (v >= 2 && v <= 16) stages = v;
+        }
+        p.tma_stages = stages;
+        p.tma_smem = vec_smem_bytes(r, p.vec_warps, stages);
+        for (int fwd = 0; fwd < 2; ++fwd) {
+            const void* fn = fwd ? vec_ptr<true>(r, p.vec_warps) : vec_ptr<false>(r, p.vec_warps);
+            if (!fn) throw Status(SF_ERR_INVALID, "vector stencil not compiled");
+            SF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(p.tma_smem)));
+        }
+        return;
+    }
     // 3 planes in flight measured best on B200 (c2: S=3 86.6 us, S=4 101 us,
     // S=8 161 us per launch: occupancy beats depth); at least 2 CTAs per SM
     int stages = 3;
@@ -556,6 +618,13 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
             for (int k = 0; k < 3; ++k) T.tc[k] = p.ac.tc[k];
             T.c0 = p.ac.c0;
             for (int j = 0; j < 8; ++j) T.cj[j] = p.ac.cj[j];
+            if (p.use_vec) {
+                if (p.ac.forward)
+                    launch_vec<true>(p.ac.radius, p.vec_warps, p.grid3, p.tma_smem, p.stream, T);
+                else
+                    launch_vec<false>(p.ac.radius, p.vec_warps, p.grid3, p.tma_smem, p.stream, T);
+                return;
+            }
             if (p.ac.forward)
                 launch_tma<true>(p.ac.radius, p.tile_nx, p.grid3, p.tma_smem, p.stream, T);
             else
@@ -926,13 +995,18 @@ int max_tile_nx(int r) { return r <= 4 ? 4 : 2; }
 // that put at least one full wave on the machine.
 void set_grid(Plan& p) {
     const int r = p.ac.radius;
-    const int64_t wx = 32 * p.tile_nx;
-    const int64_t gx = (p.n[2] + wx - 1) / wx, gy = (p.n[1] + p.tile_ty - 1) / p.tile_ty;
+    const int64_t wx = p.use_vec ? 64 : 32 * p.tile_nx;
+    const int64_t wy = p.use_vec ? 2 * p.vec_warps : p.tile_ty;
+    const int64_t gx = (p.n[2] + wx - 1) / wx, gy = (p.n[1] + wy - 1) / wy;
     const int64_t nz = p.z1 - p.z0;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
     int per_sm = 0;
-    if (p.use_tma) {
+    if (p.use_vec) {
+        const void* fn = p.ac.forward ? vec_ptr<true>(r, p.vec_warps) : vec_ptr<false>(r, p.vec_warps);
+        if (fn)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.vec_warps, p.tma_smem);
+    } else if (p.use_tma) {
         const void* fn = p.ac.forward ? tma_ptr<true>(r, p.tile_nx) : tma_ptr<false>(r, p.tile_nx);
         if (fn) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, p.tma_smem);
     } else {
@@ -1003,6 +1077,15 @@ void enable_tma(Plan& p) {
     if (p.ndim != 3) return;
     if (const char* env = std::getenv("SF_NO_TMA"))
         if (env[0] == '1') return;
+    const char* vec = std::getenv("SF_VEC");
+    if (vec && vec[0] == '1' && p.ac.radius <= 4) {
+        p.use_vec = true;
+        if (const char* w = std::getenv("SF_VEC_WARPS")) p.vec_warps = std::atoi(w) == 4 ? 4 : 8;
+        setup_tma(p);
+        p.use_tma = true;
+        set_grid(p);
+        return;
+    }
     const char* force = std::getenv("SF_TMA");
     if (p.ac.radius > 3 && !(force && force[0] == '1')) return;
     if (p.ac.radius > 4 && !std::getenv("SF_TILE")) p.tile_nx = 1;
