@@ -405,7 +405,7 @@ def run_b200_arm(args, world, rank, local):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_kind,
-                     "kernel": f"acoustic3d_kernel<R={r}> avg launch {stencil_launch_ms * 1e3:.1f} us",
+                     "kernel": f"3D stencil (radius {r}) avg launch {stencil_launch_ms * 1e3:.1f} us",
                      "alg_bytes_per_launch": alg_bytes},
         "stencil_share": sten_ms / tot_ms if tot_ms > 0 else None,
         "cpu_baseline": base,

@@ -1065,21 +1065,26 @@ void choose_geometry(Plan& p) {
     set_grid(p);
 }
 
-// Switch a 3D plan to the TMA pipeline once its slots exist (SF_NO_TMA=1
-// keeps the per-thread-load kernel, for comparisons).
+// Switch a 3D plan to a TMA pipeline once its slots exist.
 //
-// Used for radius <= 3 (space order <= 6), where the stencil is memory-bound
-// and the pipeline wins (c2 order 4: 86.6 us vs 111 us per launch). At
-// higher orders the kernel is issue-bound, the ring's 2R extra LDS per point
-// cost more than the register queue's moves (c3 order 16: 1578 vs 1027 us),
-// so the per-thread-load kernel stays (SF_TMA=1 forces the pipeline).
+// Radius <= 4 (space order <= 8): the vectorised TMA kernel (4 points per
+// thread, LDS.128 neighbours). Measured per launch on B200 against the
+// scalar TMA kernel / per-thread-load kernel: c2 order 4 81.0 vs 86.6 vs
+// 111 us; c3 order 4 412 vs 505 vs 555 us; order 6 484 vs 584 vs 605 us;
+// order 8 533 (8 warps) vs 851 vs 708 us. 4-warp CTAs for radius <= 3,
+// 8-warp CTAs at radius 4. Above radius 4 the ring no longer fits next to a
+// useful occupancy and the per-thread-load kernel with its register queue
+// stays. Overrides: SF_VEC=0 (scalar TMA / per-thread loads), SF_VEC_WARPS,
+// SF_TMA=1 (scalar TMA at any order), SF_NO_TMA=1 (per-thread loads only).
 void enable_tma(Plan& p) {
     if (p.ndim != 3) return;
     if (const char* env = std::getenv("SF_NO_TMA"))
         if (env[0] == '1') return;
     const char* vec = std::getenv("SF_VEC");
-    if (vec && vec[0] == '1' && p.ac.radius <= 4) {
+    const bool vec_on = !(vec && vec[0] == '0');
+    if (vec_on && p.ac.radius <= 4) {
         p.use_vec = true;
+        p.vec_warps = p.ac.radius <= 3 ? 4 : 8;
         if (const char* w = std::getenv("SF_VEC_WARPS")) p.vec_warps = std::atoi(w) == 4 ? 4 : 8;
         setup_tma(p);
         p.use_tma = true;
