@@ -120,6 +120,11 @@ struct sf_plan {
     int tma_stages = 4;
     size_t tma_smem = 0;
     CUtensorMap tm_cur[3], tm_pme[3], tm_m, tm_eta;
+    // FWI: history (nt+2 levels), adjoint slots v, gradient
+    CUtensorMap tm_hist_cur, tm_hist_pme, tm_v_cur[3], tm_v_pme[3], tm_grad;
+    dim3 grid_grad;          // GRAD launches use 4-warp CTAs (6 boxes per stage)
+    int zchunk_grad = 0;
+    size_t smem_grad = 0;
     std::map<std::pair<int64_t, int64_t>, cudaGraphExec_t> graphs;
     std::vector<std::string> arg_names;
     std::vector<int64_t> arg_bytes;
@@ -401,12 +406,35 @@ const void* vec_ptr(int r, int warps) {
 #undef SF_V
 }
 
-size_t vec_smem_bytes(int r, int warps, int stages) {
+size_t vec_smem_bytes(int r, int warps, int stages, int npme = 3) {
     const int ra = (r + 3) / 4 * 4;
     const int wb = 64 + 2 * ra, h = 2 * warps + 2 * r;
     const int cur = (wb * h * 4 + 127) / 128 * 128;
     const int pme = (64 * 2 * warps * 4 + 127) / 128 * 128;
-    return 256 + static_cast<size_t>(2 * r + stages) * cur + static_cast<size_t>(stages) * 3 * pme;
+    return 256 + static_cast<size_t>(2 * r + stages) * cur +
+           static_cast<size_t>(stages) * npme * pme;
+}
+
+// FWI adjoint + gradient, vectorised: 4-warp CTAs (6 boxes per stage)
+const void* vec_grad_ptr(int r) {
+    switch (r) {
+        case 1: return reinterpret_cast<const void*>(&acoustic3d_vec_kernel<1, false, 4, true>);
+        case 2: return reinterpret_cast<const void*>(&acoustic3d_vec_kernel<2, false, 4, true>);
+        case 3: return reinterpret_cast<const void*>(&acoustic3d_vec_kernel<3, false, 4, true>);
+        case 4: return reinterpret_cast<const void*>(&acoustic3d_vec_kernel<4, false, 4, true>);
+        default: return nullptr;
+    }
+}
+
+void launch_vec_grad(int r, dim3 g, size_t smem, cudaStream_t st, const TmaStencilArgs& A) {
+    const dim3 b(128);
+    switch (r) {
+        case 1: acoustic3d_vec_kernel<1, false, 4, true><<<g, b, smem, st>>>(A); return;
+        case 2: acoustic3d_vec_kernel<2, false, 4, true><<<g, b, smem, st>>>(A); return;
+        case 3: acoustic3d_vec_kernel<3, false, 4, true><<<g, b, smem, st>>>(A); return;
+        case 4: acoustic3d_vec_kernel<4, false, 4, true><<<g, b, smem, st>>>(A); return;
+        default: throw Status(SF_ERR_INVALID, "vector gradient stencil compiled for radius <= 4");
+    }
 }
 
 template <bool FWD>
@@ -441,14 +469,19 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 // 3D map over one padded field: dims (n2, n1, n0), row/plane strides in
 // bytes (multiples of 16 by the 32-float pitch), box (bx, by, 1).
-void make_tensor_map(CUtensorMap* map, const Plan& p, const float* base, uint32_t bx, uint32_t by) {
-    cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.n[2]), static_cast<cuuint64_t>(p.n[1]),
-                          static_cast<cuuint64_t>(p.n[0])};
-    cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.pitch) * 4,
-                             static_cast<cuuint64_t>(p.plane) * 4};
-    cuuint32_t box[3] = {bx, by, 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+// 4D map over `levels` consecutive padded fields (a time slot: 1 level; the
+// FWI history: nt+2): dims (n2, n1, n0, levels), strides in bytes (16-byte
+// multiples by the 32-float pitch), box (bx, by, 1, 1).
+void make_tensor_map(CUtensorMap* map, const Plan& p, const float* base, uint32_t bx, uint32_t by,
+                     int64_t levels = 1) {
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(p.n[2]), static_cast<cuuint64_t>(p.n[1]),
+                          static_cast<cuuint64_t>(p.n[0]), static_cast<cuuint64_t>(levels)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(p.pitch) * 4,
+                             static_cast<cuuint64_t>(p.plane) * 4,
+                             static_cast<cuuint64_t>(p.slot_elems) * 4};
+    cuuint32_t box[4] = {bx, by, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                                       const_cast<float*>(base), dims, strides, box, es,
                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -464,12 +497,23 @@ void setup_tma(Plan& p) {
                                                         : tma_box_width(r, nx));
     const uint32_t ty = static_cast<uint32_t>(p.use_vec ? 2 * p.vec_warps : 8);
     const uint32_t tx = static_cast<uint32_t>(p.use_vec ? 64 : 32 * nx);
+    const uint32_t cy = ty + static_cast<uint32_t>(2 * r);
     for (int s = 0; s < 3; ++s) {
-        make_tensor_map(&p.tm_cur[s], p, p.slot[s], wb, ty + static_cast<uint32_t>(2 * r));
-        make_tensor_map(&p.tm_pme[s], p, p.slot[s], tx, ty);
+        if (p.slot[s]) {
+            make_tensor_map(&p.tm_cur[s], p, p.slot[s], wb, cy);
+            make_tensor_map(&p.tm_pme[s], p, p.slot[s], tx, ty);
+        }
     }
     make_tensor_map(&p.tm_m, p, p.m, tx, ty);
     make_tensor_map(&p.tm_eta, p, p.eta, tx, ty);
+    if (p.kind == Plan::FWI) {
+        make_tensor_map(&p.tm_hist_cur, p, p.hist, wb, cy, p.nt + 2);
+        make_tensor_map(&p.tm_hist_pme, p, p.hist, tx, ty, p.nt + 2);
+        for (int s = 0; s < 3; ++s) {
+            make_tensor_map(&p.tm_v_cur[s], p, p.v[s], wb, cy);
+            make_tensor_map(&p.tm_v_pme[s], p, p.v[s], tx, ty);
+        }
+    }
     if (p.use_vec) {
         int stages = 3;
         while (stages > 2 && vec_smem_bytes(r, p.vec_warps, stages) * 2 > 226 * 1024) --stages;
@@ -484,6 +528,12 @@ void setup_tma(Plan& p) {
             if (!fn) throw Status(SF_ERR_INVALID, "vector stencil not compiled");
             SF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(p.tma_smem)));
+        }
+        if (p.kind == Plan::FWI) {
+            make_tensor_map(&p.tm_grad, p, p.grad, 64, 8);
+            p.smem_grad = vec_smem_bytes(r, 4, stages, 6);
+            SF_CUDA(cudaFuncSetAttribute(vec_grad_ptr(r), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(p.smem_grad)));
         }
         return;
     }
@@ -586,51 +636,85 @@ StencilArgs stencil_args(const Plan& p, float* out, const float* cur, const floa
     return A;
 }
 
-int slot_index(const Plan& p, const float* f) {
-    for (int s = 0; s < 3; ++s)
-        if (p.slot[s] == f) return s;
-    return -1;
+// Tensor maps (halo'd box + plain box) and level addressing `f`.
+struct MapSel {
+    const CUtensorMap* cur = nullptr;
+    const CUtensorMap* pme = nullptr;
+    int level = 0;
+};
+
+bool map_for(const Plan& p, const float* f, MapSel* m) {
+    for (int s = 0; s < 3; ++s) {
+        if (p.slot[s] && f == p.slot[s]) {
+            *m = {&p.tm_cur[s], &p.tm_pme[s], 0};
+            return true;
+        }
+        if (p.v[s] && f == p.v[s]) {
+            *m = {&p.tm_v_cur[s], &p.tm_v_pme[s], 0};
+            return true;
+        }
+    }
+    if (p.hist && f >= p.hist) {
+        const int64_t d = f - p.hist;
+        if (d % p.slot_elems == 0 && d / p.slot_elems < p.nt + 2) {
+            *m = {&p.tm_hist_cur, &p.tm_hist_pme, static_cast<int>(d / p.slot_elems)};
+            return true;
+        }
+    }
+    return false;
 }
 
 void launch_stencil(const Plan& p, float* out, const float* cur, const float* prev,
                     float* grad = nullptr, const float* uhist = nullptr) {
-    if (p.use_tma && !grad && p.ndim == 3) {
-        const int sc = slot_index(p, cur), sp = slot_index(p, prev);
-        if (sc >= 0 && sp >= 0) {
-            TmaStencilArgs T;
-            std::memset(&T, 0, sizeof T);
-            T.cur = p.tm_cur[sc];
-            T.prev = p.tm_pme[sp];
-            T.m = p.tm_m;
-            T.eta = p.tm_eta;
-            T.out = out;
-            T.pitch = static_cast<int>(p.pitch);
-            T.plane = static_cast<int>(p.plane);
-            T.n0 = static_cast<int>(p.n[0]);
-            T.n1 = static_cast<int>(p.n[1]);
-            T.n2 = static_cast<int>(p.n[2]);
-            T.zchunk = p.zchunk;
-            T.z0 = p.z0;
-            T.z1 = p.z1;
-            T.stages = p.tma_stages;
-            T.ce = p.ac.ce;
-            T.cm = p.ac.cm;
-            for (int k = 0; k < 3; ++k) T.tc[k] = p.ac.tc[k];
-            T.c0 = p.ac.c0;
-            for (int j = 0; j < 8; ++j) T.cj[j] = p.ac.cj[j];
-            if (p.use_vec) {
-                if (p.ac.forward)
-                    launch_vec<true>(p.ac.radius, p.vec_warps, p.grid3, p.tma_smem, p.stream, T);
-                else
-                    launch_vec<false>(p.ac.radius, p.vec_warps, p.grid3, p.tma_smem, p.stream, T);
-                return;
-            }
-            if (p.ac.forward)
-                launch_tma<true>(p.ac.radius, p.tile_nx, p.grid3, p.tma_smem, p.stream, T);
-            else
-                launch_tma<false>(p.ac.radius, p.tile_nx, p.grid3, p.tma_smem, p.stream, T);
+    MapSel mc, mp, mo, mu;
+    const bool maps = p.use_tma && p.ndim == 3 && map_for(p, cur, &mc) && map_for(p, prev, &mp);
+    const bool grad_ok = !grad || (p.use_vec && map_for(p, out, &mo) && map_for(p, uhist, &mu));
+    if (maps && grad_ok) {
+        TmaStencilArgs T;
+        std::memset(&T, 0, sizeof T);
+        T.cur = *mc.cur;
+        T.prev = *mp.pme;
+        T.lv_cur = mc.level;
+        T.lv_prev = mp.level;
+        T.m = p.tm_m;
+        T.eta = p.tm_eta;
+        T.out = out;
+        T.pitch = static_cast<int>(p.pitch);
+        T.plane = static_cast<int>(p.plane);
+        T.n0 = static_cast<int>(p.n[0]);
+        T.n1 = static_cast<int>(p.n[1]);
+        T.n2 = static_cast<int>(p.n[2]);
+        T.zchunk = p.zchunk;
+        T.z0 = p.z0;
+        T.z1 = p.z1;
+        T.stages = p.tma_stages;
+        T.ce = p.ac.ce;
+        T.cm = p.ac.cm;
+        for (int k = 0; k < 3; ++k) T.tc[k] = p.ac.tc[k];
+        T.c0 = p.ac.c0;
+        for (int j = 0; j < 8; ++j) T.cj[j] = p.ac.cj[j];
+        if (grad) {
+            T.old = *mo.pme;
+            T.uh = *mu.pme;
+            T.lv_uh = mu.level;
+            T.grad = p.tm_grad;
+            T.gradp = grad;
+            T.zchunk = p.zchunk_grad;
+            launch_vec_grad(p.ac.radius, p.grid_grad, p.smem_grad, p.stream, T);
             return;
         }
+        if (p.use_vec) {
+            if (p.ac.forward)
+                launch_vec<true>(p.ac.radius, p.vec_warps, p.grid3, p.tma_smem, p.stream, T);
+            else
+                launch_vec<false>(p.ac.radius, p.vec_warps, p.grid3, p.tma_smem, p.stream, T);
+            return;
+        }
+        if (p.ac.forward)
+            launch_tma<true>(p.ac.radius, p.tile_nx, p.grid3, p.tma_smem, p.stream, T);
+        else
+            launch_tma<false>(p.ac.radius, p.tile_nx, p.grid3, p.tma_smem, p.stream, T);
+        return;
     }
     StencilArgs A = stencil_args(p, out, cur, prev);
     A.grad = grad;
@@ -993,29 +1077,14 @@ int max_tile_nx(int r) { return r <= 4 ? 4 : 2; }
 // (#SM x resident CTAs/SM), each CTA costs its chunk length plus the 2R-plane
 // queue warm-up, so minimise waves(gz) * (chunk(gz) + 2R) over the chunkings
 // that put at least one full wave on the machine.
-void set_grid(Plan& p) {
+// Chunking cost model for one kernel shape (tile wx x wy, resident CTAs/SM).
+void chunk_grid(const Plan& p, int64_t wx, int64_t wy, int per_sm, dim3* grid, int* zchunk) {
     const int r = p.ac.radius;
-    const int64_t wx = p.use_vec ? 64 : 32 * p.tile_nx;
-    const int64_t wy = p.use_vec ? 2 * p.vec_warps : p.tile_ty;
     const int64_t gx = (p.n[2] + wx - 1) / wx, gy = (p.n[1] + wy - 1) / wy;
     const int64_t nz = p.z1 - p.z0;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
-    int per_sm = 0;
-    if (p.use_vec) {
-        const void* fn = p.ac.forward ? vec_ptr<true>(r, p.vec_warps) : vec_ptr<false>(r, p.vec_warps);
-        if (fn)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.vec_warps, p.tma_smem);
-    } else if (p.use_tma) {
-        const void* fn = p.ac.forward ? tma_ptr<true>(r, p.tile_nx) : tma_ptr<false>(r, p.tile_nx);
-        if (fn) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, p.tma_smem);
-    } else {
-        const void* fn = p.ac.forward ? acoustic3d_ptr<true, false>(r, p.tile_nx, p.tile_ty)
-                                      : acoustic3d_ptr<false, false>(r, p.tile_nx, p.tile_ty);
-        if (fn) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.tile_ty, 0);
-    }
     if (per_sm < 1) per_sm = 1;
-    p.resident = per_sm;
     const int64_t slots = static_cast<int64_t>(sms) * per_sm;
     double best_cost = 1e30;
     int64_t best_gz = 1;
@@ -1031,9 +1100,35 @@ void set_grid(Plan& p) {
         }
     }
     const int64_t zc = (nz + best_gz - 1) / best_gz;
-    p.zchunk = static_cast<int>(zc);
-    p.grid3 = dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy),
-                   static_cast<unsigned>((nz + zc - 1) / zc));
+    *zchunk = static_cast<int>(zc);
+    *grid = dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy),
+                 static_cast<unsigned>((nz + zc - 1) / zc));
+}
+
+void set_grid(Plan& p) {
+    const int r = p.ac.radius;
+    const int64_t wx = p.use_vec ? 64 : 32 * p.tile_nx;
+    const int64_t wy = p.use_vec ? 2 * p.vec_warps : p.tile_ty;
+    int per_sm = 0;
+    if (p.use_vec) {
+        const void* fn = p.ac.forward ? vec_ptr<true>(r, p.vec_warps) : vec_ptr<false>(r, p.vec_warps);
+        if (fn)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.vec_warps, p.tma_smem);
+    } else if (p.use_tma) {
+        const void* fn = p.ac.forward ? tma_ptr<true>(r, p.tile_nx) : tma_ptr<false>(r, p.tile_nx);
+        if (fn) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, p.tma_smem);
+    } else {
+        const void* fn = p.ac.forward ? acoustic3d_ptr<true, false>(r, p.tile_nx, p.tile_ty)
+                                      : acoustic3d_ptr<false, false>(r, p.tile_nx, p.tile_ty);
+        if (fn) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.tile_ty, 0);
+    }
+    p.resident = per_sm;
+    chunk_grid(p, wx, wy, per_sm, &p.grid3, &p.zchunk);
+    if (p.kind == Plan::FWI && p.use_vec) {
+        int g = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g, vec_grad_ptr(r), 128, p.smem_grad);
+        chunk_grid(p, 64, 8, g, &p.grid_grad, &p.zchunk_grad);
+    }
 }
 
 // Default tile: the NX <= max that wastes the fewest lanes on the a2 extent
@@ -1557,6 +1652,7 @@ int sf_fwi_plan_create(const sf_acoustic_desc* d, int device, sf_plan** out) {
             static_cast<size_t>(levels * p->slot_elems + sfb::field_slack(*p)));
         for (int s = 0; s < 3; ++s) p->v[s] = sfb::alloc_field(*p);
         p->grad = sfb::alloc_field(*p);
+        sfb::enable_tma(*p);
         p->arg_names.clear();
         p->arg_bytes.clear();
         SF_CUDA(cudaStreamSynchronize(p->stream));

@@ -70,12 +70,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
-                                            uint64_t* bar) {
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            int w, uint64_t* bar) {
     asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
         : "memory");
 }
 
@@ -136,10 +136,10 @@ __global__ void __launch_bounds__(32 * TY) acoustic3d_tma_kernel(const __grid_co
         uint64_t* b = &bar[i % S];
         const int z = zb + i;
         mbar_arrive_expect_tx(b, group_bytes);
-        tma_load_3d(cur_slot(z + R), &A.cur, x0 - RA, y0 - R, z + R, b);
-        tma_load_3d(pme_slot(i, 0), &A.prev, x0, y0, z, b);
-        tma_load_3d(pme_slot(i, 1), &A.m, x0, y0, z, b);
-        tma_load_3d(pme_slot(i, 2), &A.eta, x0, y0, z, b);
+        tma_load_4d(cur_slot(z + R), &A.cur, x0 - RA, y0 - R, z + R, A.lv_cur, b);
+        tma_load_4d(pme_slot(i, 0), &A.prev, x0, y0, z, A.lv_prev, b);
+        tma_load_4d(pme_slot(i, 1), &A.m, x0, y0, z, 0, b);
+        tma_load_4d(pme_slot(i, 2), &A.eta, x0, y0, z, 0, b);
     };
 
     if (tid == 0) {
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(32 * TY) acoustic3d_tma_kernel(const __grid_co
         // prologue: planes zb-R .. zb+R-1 of cur on the extra barrier
         mbar_arrive_expect_tx(&bar[S], 2 * R * L::CUR_FLOATS * 4);
         for (int j = 0; j < 2 * R; ++j)
-            tma_load_3d(cur_slot(zb - R + j), &A.cur, x0 - RA, y0 - R, zb - R + j, &bar[S]);
+            tma_load_4d(cur_slot(zb - R + j), &A.cur, x0 - RA, y0 - R, zb - R + j, A.lv_cur, &bar[S]);
         for (int i = 0; i < S && i < nit; ++i) issue_group(i);
     }
 
