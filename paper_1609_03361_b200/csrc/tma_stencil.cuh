@@ -29,12 +29,19 @@
 
 namespace sfb {
 
+// All maps are 4D (a2, a1, a0, level): a time slot is a 1-level map, the
+// FWI wavefield history an (nt+2)-level one; lv_* select the level.
 struct TmaStencilArgs {
-    CUtensorMap cur;   // box (WB, TY+2R, 1) at (x0-RA, y0-R, z)
-    CUtensorMap prev;  // box (32*NX, TY, 1)
-    CUtensorMap m;     // box (32*NX, TY, 1)
-    CUtensorMap eta;   // box (32*NX, TY, 1)
+    CUtensorMap cur;   // box (WB, TY+2R, 1, 1) at (x0-RA, y0-R, z, lv_cur)
+    CUtensorMap prev;  // box (TX, TY, 1, 1)
+    CUtensorMap m;     // box (TX, TY, 1, 1)
+    CUtensorMap eta;   // box (TX, TY, 1, 1)
+    CUtensorMap old;   // GRAD: the output slot before it is overwritten (v(t+2))
+    CUtensorMap uh;    // GRAD: forward history, level lv_uh = u(t+1)
+    CUtensorMap grad;  // GRAD: gradient accumulator
     float* out;
+    float* gradp;
+    int lv_cur, lv_prev, lv_uh;
     int pitch, plane;  // elements
     int n0, n1, n2;
     int zchunk;
