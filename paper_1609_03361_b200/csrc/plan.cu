@@ -1179,8 +1179,10 @@ void enable_tma(Plan& p) {
     const bool vec_on = !(vec && vec[0] == '0');
     if (vec_on && p.ac.radius <= 4) {
         p.use_vec = true;
-        p.vec_warps = p.ac.radius <= 3 ? 4 : 8;
-        if (const char* w = std::getenv("SF_VEC_WARPS")) p.vec_warps = std::atoi(w) == 4 ? 4 : 8;
+        // FWI: one set of maps serves the forward and the 4-warp gradient kernel
+        p.vec_warps = (p.ac.radius <= 3 || p.kind == Plan::FWI) ? 4 : 8;
+        if (const char* w = std::getenv("SF_VEC_WARPS"))
+            if (p.kind != Plan::FWI) p.vec_warps = std::atoi(w) == 4 ? 4 : 8;
         setup_tma(p);
         p.use_tma = true;
         set_grid(p);
