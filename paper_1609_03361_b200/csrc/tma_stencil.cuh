@@ -68,7 +68,7 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 }
 
 // Bounded wait: a transaction count that never completes (a box/byte-count
-// mismatch) traps after ~2^26 suspended polls instead of hanging the GPU.
+// mismatch) traps after ~2^24 suspended polls instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t done = 0;
     for (uint32_t spins = 0;; ++spins) {
@@ -80,7 +80,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
         if (done) return;
-        if (spins > (1u << 26)) __trap();
+        if (spins > (1u << 24)) __trap();
     }
 }
 
