@@ -100,6 +100,8 @@ struct sf_plan {
     // device mirrors
     float* slot[3] = {nullptr, nullptr, nullptr};
     float* staging = nullptr;  // dense copy of one field for host transfers
+    float* dscratch[2] = {nullptr, nullptr};  // diffusion: second buffer pair (temporal blocking)
+    bool diffusion_tb = true;
     float* m = nullptr;
     float* eta = nullptr;
     sfb::PointSet src, rec;
@@ -881,7 +883,7 @@ void launch_inject_sample(const Plan& p, const PointSet& inj, const PointSet& sm
 }
 
 int64_t launches_per_step_of(const Plan& p) {
-    if (p.kind == Plan::DIFFUSION) return 1;
+    if (p.kind == Plan::DIFFUSION) return 1;  // per step without temporal blocking
     if (p.nccl_comm && (p.has_lower || p.has_upper)) return 3;
     const PointSet& inj = p.ac.forward ? p.src : p.rec;
     const PointSet& smp = p.ac.forward ? p.rec : p.src;
@@ -981,6 +983,87 @@ void enqueue_diffusion_step(Plan& p, int64_t t) {
     launch_diffusion_r(p.dc.radius, g, b, p.stream, A);
 }
 
+// Temporally blocked diffusion (diffusion_tb_kernel): TMAX = 8/R steps per
+// launch on 64x64 tiles, (64 + 16)^2-float ping-pong buffers.
+constexpr int kTbTile = 64;
+
+template <int R>
+void launch_diffusion_tb_t(dim3 g, cudaStream_t st, const DiffusionTBArgs& A) {
+    constexpr int TMAX = 8 / R > 0 ? 8 / R : 1;
+    constexpr int SW = kTbTile + 2 * TMAX * R;
+    const size_t smem = 2 * SW * SW * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+        SF_CUDA(cudaFuncSetAttribute(&diffusion_tb_kernel<R, kTbTile, TMAX>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+        attr = true;
+    }
+    diffusion_tb_kernel<R, kTbTile, TMAX><<<g, 256, smem, st>>>(A);
+}
+
+int diffusion_tmax(int r) { return 8 / r > 0 ? 8 / r : 1; }
+
+void launch_diffusion_tb(int r, dim3 g, cudaStream_t st, const DiffusionTBArgs& A) {
+    switch (r) {
+        case 1: return launch_diffusion_tb_t<1>(g, st, A);
+        case 2: return launch_diffusion_tb_t<2>(g, st, A);
+        case 3: return launch_diffusion_tb_t<3>(g, st, A);
+        case 4: return launch_diffusion_tb_t<4>(g, st, A);
+        case 5: return launch_diffusion_tb_t<5>(g, st, A);
+        case 6: return launch_diffusion_tb_t<6>(g, st, A);
+        case 7: return launch_diffusion_tb_t<7>(g, st, A);
+        case 8: return launch_diffusion_tb_t<8>(g, st, A);
+        default: throw Status(SF_ERR_INVALID, "radius out of range");
+    }
+}
+
+// Steps [b, e): copy both slots into the scratch pair (boundary values),
+// then alternate read/write pairs launch by launch; the final pair is copied
+// back into the slots if it is the scratch one.
+void enqueue_diffusion_tb(Plan& p, int64_t b, int64_t e) {
+    const size_t bytes = sizeof(float) * p.slot_elems;
+    for (int s = 0; s < 2; ++s)
+        SF_CUDA(cudaMemcpyAsync(p.dscratch[s], p.slot[s], bytes, cudaMemcpyDeviceToDevice, p.stream));
+    float* X[2] = {p.slot[0], p.slot[1]};
+    float* Y[2] = {p.dscratch[0], p.dscratch[1]};
+    const int tmax = diffusion_tmax(p.dc.radius);
+    dim3 g(static_cast<unsigned>((p.n[1] + kTbTile - 1) / kTbTile),
+           static_cast<unsigned>((p.n[0] + kTbTile - 1) / kTbTile));
+    bool in_x = true;
+    for (int64_t t = b; t < e;) {
+        const int T = static_cast<int>(std::min<int64_t>(tmax, e - t));
+        DiffusionTBArgs A{};
+        float* const* rd = in_x ? X : Y;
+        float* const* wr = in_x ? Y : X;
+        A.src[0] = rd[0];
+        A.src[1] = rd[1];
+        A.dst[0] = wr[0];
+        A.dst[1] = wr[1];
+        A.pitch = p.pitch;
+        A.n0 = static_cast<int>(p.n[0]);
+        A.n1 = static_cast<int>(p.n[1]);
+        A.t0 = static_cast<int>(t);
+        A.T = T;
+        A.c0 = p.dc.c0;
+        A.has_c0 = p.dc.has_c0;
+        for (int j = 0; j < 8; ++j) A.cj[j] = p.dc.cj[j];
+        launch_diffusion_tb(p.dc.radius, g, p.stream, A);
+        in_x = !in_x;
+        t += T;
+    }
+    if (!in_x)
+        for (int s = 0; s < 2; ++s)
+            SF_CUDA(cudaMemcpyAsync(p.slot[s], p.dscratch[s], bytes, cudaMemcpyDeviceToDevice,
+                                    p.stream));
+}
+
+int64_t diffusion_launches(const Plan& p, int64_t steps) {
+    if (!p.diffusion_tb) return steps;
+    const int64_t tmax = diffusion_tmax(p.dc.radius);
+    return (steps + tmax - 1) / tmax;
+}
+
 // FWI phases (config 5): forward into the HBM history, then the adjoint
 // sweep with the delayed gradient term fused into the stencil.
 void enqueue_fwi_forward(Plan& p) {
@@ -1027,6 +1110,7 @@ constexpr int64_t kStencilOnly = -1, kFwiForward = -2, kFwiAdjoint = -3;
 
 void enqueue_steps(Plan& p, int64_t b, int64_t e) {
     if (b == kStencilOnly) {
+        if (p.kind == Plan::DIFFUSION && p.diffusion_tb) return enqueue_diffusion_tb(p, 0, p.nt);
         for (int64_t k = 0; k < p.nt; ++k) {
             if (p.kind == Plan::DIFFUSION)
                 enqueue_diffusion_step(p, k);
@@ -1037,6 +1121,7 @@ void enqueue_steps(Plan& p, int64_t b, int64_t e) {
     }
     if (b == kFwiForward) return enqueue_fwi_forward(p);
     if (b == kFwiAdjoint) return enqueue_fwi_adjoint(p);
+    if (p.kind == Plan::DIFFUSION && p.diffusion_tb) return enqueue_diffusion_tb(p, b, e);
     for (int64_t k = b; k < e; ++k) {
         if (p.kind == Plan::DIFFUSION)
             enqueue_diffusion_step(p, k);
@@ -1380,6 +1465,7 @@ sf_plan::~sf_plan() {
     if (stream) cudaStreamSynchronize(stream);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (float* s : slot) sfb::dfree(s);
+    for (float* s : dscratch) sfb::dfree(s);
     sfb::dfree(staging);
     sfb::dfree(m);
     sfb::dfree(eta);
@@ -1448,6 +1534,8 @@ int sf_diffusion_plan_create(const sf_diffusion_desc* d, int device, sf_plan** o
         p->dc = sfb::diffusion_constants(sfb::Rat::make(d->alpha_num, d->alpha_den),
                                          sfb::Rat::make(d->dx_num, d->dx_den), d->order);
         for (int s = 0; s < 2; ++s) p->slot[s] = sfb::alloc_field(*p);
+        for (int s = 0; s < 2; ++s) p->dscratch[s] = sfb::alloc_field(*p);
+        if (const char* env = std::getenv("SF_DIFFUSION_TB")) p->diffusion_tb = env[0] != '0';
         p->arg_names = {"u"};
         p->arg_bytes = {2 * d->nx * d->ny * 4};
         p->launches_per_step = 1;
@@ -1625,7 +1713,9 @@ int sf_plan_time(sf_plan* p, float* total_ms, float* stencil_ms, int64_t* launch
         float ms = 0;
         SF_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
         if (total_ms) *total_ms = ms;
-        if (launches) *launches = sfb::launches_per_step_of(*p) * p->nt;
+        if (launches)
+            *launches = p->kind == sf_plan::DIFFUSION ? sfb::diffusion_launches(*p, p->nt)
+                                                      : sfb::launches_per_step_of(*p) * p->nt;
         if (stencil_ms) {
             // same steps with only the stencil launches: their summed duration
             sfb::run_steps(*p, sfb::kStencilOnly, sfb::kStencilOnly);

@@ -288,3 +288,22 @@ def test_fwi_gradient_vs_oracle(sf, port):
     assert_parity(srcs, s2)
     assert np.abs(g).max() > 0
     assert_parity(grad, g)
+
+
+@pytest.mark.parametrize("order,n,nt", [(2, 203, 37), (4, 150, 19), (8, 97, 13), (16, 70, 5)])
+def test_diffusion_temporal_blocking_vs_oracle(sf, port, order, n, nt):
+    """Temporally blocked diffusion (several steps per launch) vs the port:
+    ragged grids, step counts that are not multiples of the block depth, and
+    slots whose boundary strips differ (each level must see its own slot's
+    boundary values, as in the reference's 2-slot loop)."""
+    from fractions import Fraction
+    rng = np.random.default_rng(order)
+    u = rng.random((2, n, n)).astype(np.float32)
+    cfg = sf.DiffusionConfig(nx=n, ny=n, alpha=Fraction(1, 3), dx=Fraction(1, n - 1),
+                             dy=Fraction(1, n - 1), nt=nt, order=order)
+    b = sf.make_diffusion_operator(cfg)
+    b.u.data[...] = u
+    b.op.apply()
+    ref = u.copy()
+    port.diffusion_run(ref, order, (1, 3), (1, n - 1), nt)
+    assert_parity(b.u.data, ref)
