@@ -440,105 +440,4 @@ __global__ void __launch_bounds__(256) diffusion_kernel(const DiffusionArgs A) {
     A.out[o] = acc;
 }
 
-// ---------------------------------------------------------------------------
-// K1, temporally blocked. The 2048^2 field is L2-resident, so the one-step
-// kernel is bound by L2 and launch latency, not HBM. Here a CTA loads a
-// (TILE + 2TR)^2 patch of both slots into shared memory once, advances it T
-// steps in place (ping-pong, the valid region shrinking by R per step), and
-// writes its TILE^2 core of the last two levels: T steps per launch, 1/T of
-// the global traffic. Every value is computed by exactly the single-step
-// expression from the same neighbour values, so the result is bitwise the
-// step-by-step run. Boundary cells (outside [R, n-R)) are never updated: the
-// ping-pong buffers are loaded from the slot of matching parity so each level
-// sees its own slot's boundary values, as in the reference's 2-slot loop.
-// Launches read one buffer pair and write the other (no intra-launch
-// hazards); the plan alternates pairs.
-struct DiffusionTBArgs {
-    const float* src[2];  // pair read, indexed by level parity
-    float* dst[2];        // pair written, indexed by level parity
-    int64_t pitch;
-    int n0, n1;
-    int t0;  // level at launch start
-    int T;   // steps in this launch (<= TMAX)
-    float c0;
-    int has_c0;
-    float cj[8];
-};
-
-template <int R>
-__device__ __forceinline__ float diffusion_point(const DiffusionTBArgs& A, const float* c, int w) {
-    float acc = 0.0f;
-    bool first = true;
-    if (A.has_c0) {
-        acc = __fmul_rn(A.c0, c[0]);
-        first = false;
-    }
-#pragma unroll
-    for (int j = R; j >= 1; --j) {
-        const float t = __fmul_rn(A.cj[j - 1], c[-j]);
-        acc = first ? t : __fadd_rn(acc, t);
-        first = false;
-    }
-#pragma unroll
-    for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(A.cj[j - 1], c[j]));
-#pragma unroll
-    for (int j = R; j >= 1; --j) acc = __fadd_rn(acc, __fmul_rn(A.cj[j - 1], c[-j * w]));
-#pragma unroll
-    for (int j = 1; j <= R; ++j) acc = __fadd_rn(acc, __fmul_rn(A.cj[j - 1], c[j * w]));
-    return acc;
-}
-
-template <int R, int TILE, int TMAX>
-__global__ void __launch_bounds__(256) diffusion_tb_kernel(const DiffusionTBArgs A) {
-    constexpr int SW = TILE + 2 * TMAX * R;  // smem side
-    extern __shared__ __align__(16) float sm[];
-    float* buf[2] = {sm, sm + SW * SW};
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-    const int T = A.T;
-    const int h = T * R;
-    const int W = TILE + 2 * h;
-    const int gx0 = blockIdx.x * TILE - h;  // a1 of smem column 0
-    const int gy0 = blockIdx.y * TILE - h;  // a0 of smem row 0
-    const float* s0 = A.src[A.t0 & 1];
-    const float* s1 = A.src[(A.t0 + 1) & 1];
-    for (int y = ty; y < W; y += 8) {
-        const int gy = gy0 + y;
-        if (gy < 0 || gy >= A.n0) continue;
-        for (int x = tx; x < W; x += 32) {
-            const int gx = gx0 + x;
-            if (gx < 0 || gx >= A.n1) continue;
-            const int64_t o = static_cast<int64_t>(gy) * A.pitch + gx;
-            buf[0][y * SW + x] = __ldg(s0 + o);
-            buf[1][y * SW + x] = __ldg(s1 + o);
-        }
-    }
-    __syncthreads();
-    for (int st = 1; st <= T; ++st) {
-        const float* in = buf[(st - 1) & 1];
-        float* out = buf[st & 1];
-        // region still valid after this step, clipped to the global interior
-        const int ylo = max(st * R, R - gy0), yhi = min(W - st * R, A.n0 - R - gy0);
-        const int xlo = max(st * R, R - gx0), xhi = min(W - st * R, A.n1 - R - gx0);
-        for (int y = ylo + ty; y < yhi; y += 8)
-            for (int x = xlo + tx; x < xhi; x += 32)
-                out[y * SW + x] = diffusion_point<R>(A, in + y * SW + x, SW);
-        __syncthreads();
-    }
-    // core cells of the last two levels (interior only)
-    for (int lv = 0; lv < 2; ++lv) {
-        const int level = A.t0 + T - lv;
-        const float* b = buf[(T - lv) & 1];
-        float* d = A.dst[level & 1];
-        for (int y = h + ty; y < h + TILE; y += 8) {
-            const int gy = gy0 + y;
-            if (gy < R || gy >= A.n0 - R) continue;
-            for (int x = h + tx; x < h + TILE; x += 32) {
-                const int gx = gx0 + x;
-                if (gx < R || gx >= A.n1 - R) continue;
-                d[static_cast<int64_t>(gy) * A.pitch + gx] = b[y * SW + x];
-            }
-        }
-    }
-}
-
 } // namespace sfb

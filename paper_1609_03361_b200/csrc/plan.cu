@@ -28,6 +28,7 @@
 #include "kernels.cuh"
 #include "tma_stencil.cuh"
 #include "vec_stencil.cuh"
+#include "diffusion_tb.cuh"
 #include "sf_internal.h"
 
 namespace sfb {
@@ -102,6 +103,7 @@ struct sf_plan {
     float* staging = nullptr;  // dense copy of one field for host transfers
     float* dscratch[2] = {nullptr, nullptr};  // diffusion: second buffer pair (temporal blocking)
     bool diffusion_tb = true;
+    CUtensorMap tm_dx[2], tm_dy[2];  // diffusion: 2D maps over slots / scratch (box SW x SW)
     float* m = nullptr;
     float* eta = nullptr;
     sfb::PointSet src, rec;
@@ -990,16 +992,34 @@ constexpr int kTbTile = 64;
 template <int R>
 void launch_diffusion_tb_t(dim3 g, cudaStream_t st, const DiffusionTBArgs& A) {
     constexpr int TMAX = 8 / R > 0 ? 8 / R : 1;
-    constexpr int SW = kTbTile + 2 * TMAX * R;
-    const size_t smem = 2 * SW * SW * sizeof(float);
+    using L = TbLayout<R, kTbTile, TMAX>;
     static bool attr = false;
     if (!attr) {
         SF_CUDA(cudaFuncSetAttribute(&diffusion_tb_kernel<R, kTbTile, TMAX>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
+                                     static_cast<int>(L::smem)));
         attr = true;
     }
-    diffusion_tb_kernel<R, kTbTile, TMAX><<<g, 256, smem, st>>>(A);
+    diffusion_tb_kernel<R, kTbTile, TMAX><<<g, 256, L::smem, st>>>(A);
+}
+
+int diffusion_box(int r) {
+    const int tmax = 8 / r > 0 ? 8 / r : 1;
+    return kTbTile + 2 * ((tmax * r + 3) / 4 * 4);
+}
+
+void make_map_2d(CUtensorMap* map, const Plan& p, const float* base, uint32_t box) {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.n[1]), static_cast<cuuint64_t>(p.n[0])};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.pitch) * 4};
+    cuuint32_t bx[2] = {box, box};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = tensor_map_encoder()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                      const_cast<float*>(base), dims, strides, bx, es,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw Status(SF_ERR_CUDA, "cuTensorMapEncodeTiled (2D) failed: " + std::to_string(r));
 }
 
 int diffusion_tmax(int r) { return 8 / r > 0 ? 8 / r : 1; }
@@ -1033,11 +1053,11 @@ void enqueue_diffusion_tb(Plan& p, int64_t b, int64_t e) {
     bool in_x = true;
     for (int64_t t = b; t < e;) {
         const int T = static_cast<int>(std::min<int64_t>(tmax, e - t));
-        DiffusionTBArgs A{};
-        float* const* rd = in_x ? X : Y;
+        DiffusionTBArgs A;
+        std::memset(&A, 0, sizeof A);
         float* const* wr = in_x ? Y : X;
-        A.src[0] = rd[0];
-        A.src[1] = rd[1];
+        A.src0 = in_x ? p.tm_dx[0] : p.tm_dy[0];
+        A.src1 = in_x ? p.tm_dx[1] : p.tm_dy[1];
         A.dst[0] = wr[0];
         A.dst[1] = wr[1];
         A.pitch = p.pitch;
@@ -1536,6 +1556,13 @@ int sf_diffusion_plan_create(const sf_diffusion_desc* d, int device, sf_plan** o
         for (int s = 0; s < 2; ++s) p->slot[s] = sfb::alloc_field(*p);
         for (int s = 0; s < 2; ++s) p->dscratch[s] = sfb::alloc_field(*p);
         if (const char* env = std::getenv("SF_DIFFUSION_TB")) p->diffusion_tb = env[0] != '0';
+        if (p->diffusion_tb) {
+            const uint32_t box = static_cast<uint32_t>(sfb::diffusion_box(p->dc.radius));
+            for (int s = 0; s < 2; ++s) {
+                sfb::make_map_2d(&p->tm_dx[s], *p, p->slot[s], box);
+                sfb::make_map_2d(&p->tm_dy[s], *p, p->dscratch[s], box);
+            }
+        }
         p->arg_names = {"u"};
         p->arg_bytes = {2 * d->nx * d->ny * 4};
         p->launches_per_step = 1;
