@@ -120,6 +120,7 @@ struct sf_plan {
     // TMA pipeline path (3D forward/adjoint without the FWI gradient)
     bool use_tma = false;
     bool use_vec = false;  // 4 points/thread, LDS.128 variant of the TMA pipeline
+    bool use_vecq = false; // ... with the a0 neighbours in a register queue (radius >= 5)
     int vec_warps = 8;
     int tma_stages = 4;
     size_t tma_smem = 0;
@@ -419,6 +420,43 @@ size_t vec_smem_bytes(int r, int warps, int stages, int npme = 3) {
            static_cast<size_t>(stages) * npme * pme;
 }
 
+template <bool FWD>
+const void* vecq_ptr(int r, int warps) {
+#define SF_V(RR)                                                                               \
+    case RR:                                                                                   \
+        return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 4>) \
+                          : reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 8>);
+    switch (r) {
+        SF_V(5) SF_V(6) SF_V(7) SF_V(8)
+        default: return nullptr;
+    }
+#undef SF_V
+}
+
+size_t vecq_smem_bytes(int r, int warps, int stages) {
+    const int ra = (r + 3) / 4 * 4;
+    const int cur = ((64 + 2 * ra) * (2 * warps + 2 * r) * 4 + 127) / 128 * 128;
+    const int pme = (64 * 2 * warps * 4 + 127) / 128 * 128;
+    return 256 + static_cast<size_t>(stages) * (cur + 3 * pme);
+}
+
+template <bool FWD>
+void launch_vecq(int r, int warps, dim3 g, size_t smem, cudaStream_t st, const TmaStencilArgs& A) {
+    const dim3 b(32 * warps);
+#define SF_V(RR)                                                                   \
+    case RR:                                                                       \
+        if (warps == 4)                                                            \
+            acoustic3d_vecq_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);             \
+        else                                                                       \
+            acoustic3d_vecq_kernel<RR, FWD, 8><<<g, b, smem, st>>>(A);             \
+        return;
+    switch (r) {
+        SF_V(5) SF_V(6) SF_V(7) SF_V(8)
+        default: throw Status(SF_ERR_INVALID, "queue vector stencil compiled for radius 5..8");
+    }
+#undef SF_V
+}
+
 // FWI adjoint + gradient, vectorised: 4-warp CTAs (6 boxes per stage)
 const void* vec_grad_ptr(int r) {
     switch (r) {
@@ -517,6 +555,22 @@ void setup_tma(Plan& p) {
             make_tensor_map(&p.tm_v_cur[s], p, p.v[s], wb, cy);
             make_tensor_map(&p.tm_v_pme[s], p, p.v[s], tx, ty);
         }
+    }
+    if (p.use_vecq) {
+        int stages = 4;
+        if (const char* env = std::getenv("SF_TMA_STAGES")) {
+            const int v = std::atoi(env);
+            if (v >= 2 && v <= 16) stages = v;
+        }
+        p.tma_stages = stages;
+        p.tma_smem = vecq_smem_bytes(r, p.vec_warps, stages);
+        for (int fwd = 0; fwd < 2; ++fwd) {
+            const void* fn = fwd ? vecq_ptr<true>(r, p.vec_warps) : vecq_ptr<false>(r, p.vec_warps);
+            if (!fn) throw Status(SF_ERR_INVALID, "queue vector stencil not compiled");
+            SF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(p.tma_smem)));
+        }
+        return;
     }
     if (p.use_vec) {
         int stages = 3;
@@ -672,7 +726,8 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
                     float* grad = nullptr, const float* uhist = nullptr) {
     MapSel mc, mp, mo, mu;
     const bool maps = p.use_tma && p.ndim == 3 && map_for(p, cur, &mc) && map_for(p, prev, &mp);
-    const bool grad_ok = !grad || (p.use_vec && map_for(p, out, &mo) && map_for(p, uhist, &mu));
+    const bool grad_ok =
+        !grad || (p.use_vec && !p.use_vecq && map_for(p, out, &mo) && map_for(p, uhist, &mu));
     if (maps && grad_ok) {
         TmaStencilArgs T;
         std::memset(&T, 0, sizeof T);
@@ -680,6 +735,8 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
         T.prev = *mp.pme;
         T.lv_cur = mc.level;
         T.lv_prev = mp.level;
+        T.cur_ptr = cur;  // the level's own base: queue-head loads add no level offset
+        T.level_elems = 0;
         T.m = p.tm_m;
         T.eta = p.tm_eta;
         T.out = out;
@@ -705,6 +762,13 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
             T.gradp = grad;
             T.zchunk = p.zchunk_grad;
             launch_vec_grad(p.ac.radius, p.grid_grad, p.smem_grad, p.stream, T);
+            return;
+        }
+        if (p.use_vecq) {
+            if (p.ac.forward)
+                launch_vecq<true>(p.ac.radius, p.vec_warps, p.grid3, p.tma_smem, p.stream, T);
+            else
+                launch_vecq<false>(p.ac.radius, p.vec_warps, p.grid3, p.tma_smem, p.stream, T);
             return;
         }
         if (p.use_vec) {
@@ -1215,7 +1279,11 @@ void set_grid(Plan& p) {
     const int64_t wx = p.use_vec ? 64 : 32 * p.tile_nx;
     const int64_t wy = p.use_vec ? 2 * p.vec_warps : p.tile_ty;
     int per_sm = 0;
-    if (p.use_vec) {
+    if (p.use_vecq) {
+        const void* fn = p.ac.forward ? vecq_ptr<true>(r, p.vec_warps) : vecq_ptr<false>(r, p.vec_warps);
+        if (fn)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.vec_warps, p.tma_smem);
+    } else if (p.use_vec) {
         const void* fn = p.ac.forward ? vec_ptr<true>(r, p.vec_warps) : vec_ptr<false>(r, p.vec_warps);
         if (fn)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.vec_warps, p.tma_smem);
@@ -1229,7 +1297,7 @@ void set_grid(Plan& p) {
     }
     p.resident = per_sm;
     chunk_grid(p, wx, wy, per_sm, &p.grid3, &p.zchunk);
-    if (p.kind == Plan::FWI && p.use_vec) {
+    if (p.kind == Plan::FWI && p.use_vec && !p.use_vecq) {
         int g = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g, vec_grad_ptr(r), 128, p.smem_grad);
         chunk_grid(p, 64, 8, g, &p.grid_grad, &p.zchunk_grad);
@@ -1288,6 +1356,17 @@ void enable_tma(Plan& p) {
         p.vec_warps = (p.ac.radius <= 3 || p.kind == Plan::FWI) ? 4 : 8;
         if (const char* w = std::getenv("SF_VEC_WARPS"))
             if (p.kind != Plan::FWI) p.vec_warps = std::atoi(w) == 4 ? 4 : 8;
+        setup_tma(p);
+        p.use_tma = true;
+        set_grid(p);
+        return;
+    }
+    const char* vq = std::getenv("SF_VECQ");
+    if (vec_on && p.ac.radius >= 5 && vq && vq[0] == '1') {
+        p.use_vec = true;
+        p.use_vecq = true;
+        p.vec_warps = 4;
+        if (const char* w = std::getenv("SF_VEC_WARPS")) p.vec_warps = std::atoi(w) == 8 ? 8 : 4;
         setup_tma(p);
         p.use_tma = true;
         set_grid(p);

@@ -41,6 +41,8 @@ struct TmaStencilArgs {
     CUtensorMap grad;  // GRAD: gradient accumulator
     float* out;
     float* gradp;
+    const float* cur_ptr;  // base of the cur map's field (vecq queue-head loads)
+    int64_t level_elems;   // elements per level of the cur map
     int lv_cur, lv_prev, lv_uh;
     int pitch, plane;  // elements
     int n0, n1, n2;
