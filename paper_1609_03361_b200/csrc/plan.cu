@@ -557,7 +557,7 @@ void setup_tma(Plan& p) {
         }
     }
     if (p.use_vecq) {
-        int stages = 4;
+        int stages = 3;
         if (const char* env = std::getenv("SF_TMA_STAGES")) {
             const int v = std::atoi(env);
             if (v >= 2 && v <= 16) stages = v;
@@ -1341,9 +1341,11 @@ void choose_geometry(Plan& p) {
 // 111 us; c3 order 4 412 vs 505 vs 555 us; order 6 484 vs 584 vs 605 us;
 // order 8 533 (8 warps) vs 851 vs 708 us. 4-warp CTAs for radius <= 3,
 // 8-warp CTAs at radius 4. Above radius 4 the ring no longer fits next to a
-// useful occupancy and the per-thread-load kernel with its register queue
-// stays. Overrides: SF_VEC=0 (scalar TMA / per-thread loads), SF_VEC_WARPS,
-// SF_TMA=1 (scalar TMA at any order), SF_NO_TMA=1 (per-thread loads only).
+// useful occupancy: the queue-vector kernel keeps the a0 neighbours in
+// registers (c3 order 12: 677 vs 891 us; order 16: 837 vs 1027 us for the
+// per-thread-load kernel; 4-warp CTAs, 3 stages). Overrides: SF_VEC=0 /
+// SF_VECQ=0 (scalar paths), SF_VEC_WARPS, SF_TMA=1 (scalar TMA at any order),
+// SF_NO_TMA=1 (per-thread loads only).
 void enable_tma(Plan& p) {
     if (p.ndim != 3) return;
     if (const char* env = std::getenv("SF_NO_TMA"))
@@ -1362,7 +1364,7 @@ void enable_tma(Plan& p) {
         return;
     }
     const char* vq = std::getenv("SF_VECQ");
-    if (vec_on && p.ac.radius >= 5 && vq && vq[0] == '1') {
+    if (vec_on && p.ac.radius >= 5 && !(vq && vq[0] == '0')) {
         p.use_vec = true;
         p.use_vecq = true;
         p.vec_warps = 4;
