@@ -442,7 +442,7 @@ size_t vecq_smem_bytes(int r, int warps, int stages) {
 
 template <bool FWD>
 void launch_vecq(int r, int warps, dim3 g, size_t smem, cudaStream_t st, const TmaStencilArgs& A) {
-    const dim3 b(32 * warps);
+    const dim3 b(32 * (warps + 1));  // + the TMA producer warp
 #define SF_V(RR)                                                                   \
     case RR:                                                                       \
         if (warps == 4)                                                            \
@@ -469,7 +469,7 @@ const void* vec_grad_ptr(int r) {
 }
 
 void launch_vec_grad(int r, dim3 g, size_t smem, cudaStream_t st, const TmaStencilArgs& A) {
-    const dim3 b(128);
+    const dim3 b(160);  // 4 consumer warps + the TMA producer warp
     switch (r) {
         case 1: acoustic3d_vec_kernel<1, false, 4, true><<<g, b, smem, st>>>(A); return;
         case 2: acoustic3d_vec_kernel<2, false, 4, true><<<g, b, smem, st>>>(A); return;
@@ -481,7 +481,7 @@ void launch_vec_grad(int r, dim3 g, size_t smem, cudaStream_t st, const TmaStenc
 
 template <bool FWD>
 void launch_vec(int r, int warps, dim3 g, size_t smem, cudaStream_t st, const TmaStencilArgs& A) {
-    const dim3 b(32 * warps);
+    const dim3 b(32 * (warps + 1));  // + the TMA producer warp
 #define SF_V(RR)                                                                   \
     case RR:                                                                       \
         if (warps == 4)                                                            \
@@ -1282,11 +1282,13 @@ void set_grid(Plan& p) {
     if (p.use_vecq) {
         const void* fn = p.ac.forward ? vecq_ptr<true>(r, p.vec_warps) : vecq_ptr<false>(r, p.vec_warps);
         if (fn)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.vec_warps, p.tma_smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * (p.vec_warps + 1),
+                                                          p.tma_smem);
     } else if (p.use_vec) {
         const void* fn = p.ac.forward ? vec_ptr<true>(r, p.vec_warps) : vec_ptr<false>(r, p.vec_warps);
         if (fn)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.vec_warps, p.tma_smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * (p.vec_warps + 1),
+                                                          p.tma_smem);
     } else if (p.use_tma) {
         const void* fn = p.ac.forward ? tma_ptr<true>(r, p.tile_nx) : tma_ptr<false>(r, p.tile_nx);
         if (fn) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, p.tma_smem);
@@ -1299,7 +1301,7 @@ void set_grid(Plan& p) {
     chunk_grid(p, wx, wy, per_sm, &p.grid3, &p.zchunk);
     if (p.kind == Plan::FWI && p.use_vec && !p.use_vecq) {
         int g = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g, vec_grad_ptr(r), 128, p.smem_grad);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g, vec_grad_ptr(r), 160, p.smem_grad);
         chunk_grid(p, 64, 8, g, &p.grid_grad, &p.zchunk_grad);
     }
 }
