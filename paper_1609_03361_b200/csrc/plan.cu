@@ -442,7 +442,7 @@ size_t vecq_smem_bytes(int r, int warps, int stages) {
 
 template <bool FWD>
 void launch_vecq(int r, int warps, dim3 g, size_t smem, cudaStream_t st, const TmaStencilArgs& A) {
-    const dim3 b(32 * (warps + 1));  // + the TMA producer warp
+    const dim3 b(32 * warps);
 #define SF_V(RR)                                                                   \
     case RR:                                                                       \
         if (warps == 4)                                                            \
@@ -1282,8 +1282,7 @@ void set_grid(Plan& p) {
     if (p.use_vecq) {
         const void* fn = p.ac.forward ? vecq_ptr<true>(r, p.vec_warps) : vecq_ptr<false>(r, p.vec_warps);
         if (fn)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * (p.vec_warps + 1),
-                                                          p.tma_smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.vec_warps, p.tma_smem);
     } else if (p.use_vec) {
         const void* fn = p.ac.forward ? vec_ptr<true>(r, p.vec_warps) : vec_ptr<false>(r, p.vec_warps);
         if (fn)
