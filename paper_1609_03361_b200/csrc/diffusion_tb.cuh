@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256) diffusion_tb_kernel(const __grid_constant
     float* buf[2] = {reinterpret_cast<float*>(smraw + 128),
                      reinterpret_cast<float*>(smraw + 128) + SW * SW};
     const int tid = threadIdx.x;
-    const int tx = tid & 31, ty = tid >> 5;  // 32 x 8
+    const int tx = tid & 31, ty = tid >> 5;  // 32 x 8 (loads / stores)
     const int T = A.T;
     const int gx0 = blockIdx.x * TILE - HA;  // a1 of smem column 0
     const int gy0 = blockIdx.y * TILE - HA;  // a0 of smem row 0
@@ -98,17 +98,80 @@ __global__ void __launch_bounds__(256) diffusion_tb_kernel(const __grid_constant
         tma_load_2d(buf[1], (A.t0 & 1) ? &A.src0 : &A.src1, gx0, gy0, bar);
     }
     mbar_wait(bar, 0);
+    // Each thread updates 4 consecutive a1 cells per visit: one aligned
+    // (4 + 2RA)-float window (LDS.128s) gives every a1 neighbour, one
+    // LDS.128 per a0 row offset gives the a0 neighbours of all four.
+    constexpr int RA = (R + 3) / 4 * 4;
+    const int lx = tid & 15, ly = tid >> 4;  // 16 vectors x 16 rows per pass
     for (int st = 1; st <= T; ++st) {
         const float* in = buf[(st - 1) & 1];
         float* out = buf[st & 1];
-        // cells still valid after this step (core grown by (T - st) R),
-        // clipped to the global interior
+        // cells still valid after this step (core grown by (T - st) R)
         const int grow = HA - (T - st) * R;
-        const int ylo = max(grow, R - gy0), yhi = min(SW - grow, A.n0 - R - gy0);
-        const int xlo = max(grow, R - gx0), xhi = min(SW - grow, A.n1 - R - gx0);
-        for (int y = ylo + ty; y < yhi; y += 8)
-            for (int x = xlo + tx; x < xhi; x += 32)
-                out[y * SW + x] = diffusion_point<R>(A, in + y * SW + x, SW);
+        // global interior in smem coordinates
+        const int iy0 = R - gy0, iy1 = A.n0 - R - gy0;
+        const int ix0 = R - gx0, ix1 = A.n1 - R - gx0;
+        const int ylo = max(grow, iy0), yhi = min(SW - grow, iy1);
+        const int xlo = max(grow, ix0) & ~3, xhi = min(SW - grow, ix1);
+        for (int y = ylo + ly; y < yhi; y += 16) {
+            for (int x = xlo + 4 * lx; x < xhi; x += 64) {
+                const float* c = in + y * SW + x;
+                float win[4 + 2 * RA];
+#pragma unroll
+                for (int q = 0; q < (4 + 2 * RA) / 4; ++q) {
+                    const float4 w = *reinterpret_cast<const float4*>(c - RA + 4 * q);
+                    win[4 * q] = w.x;
+                    win[4 * q + 1] = w.y;
+                    win[4 * q + 2] = w.z;
+                    win[4 * q + 3] = w.w;
+                }
+                float acc[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    // first emitted term: the centre when its weight is
+                    // nonzero, else the a1 neighbour at offset -R
+                    const float t = __fmul_rn(A.cj[R - 1], win[RA + k - R]);
+                    acc[k] = A.has_c0 ? __fadd_rn(__fmul_rn(A.c0, win[RA + k]), t) : t;
+                }
+#pragma unroll
+                for (int j = R - 1; j >= 1; --j)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        acc[k] = __fadd_rn(acc[k], __fmul_rn(A.cj[j - 1], win[RA + k - j]));
+#pragma unroll
+                for (int j = 1; j <= R; ++j)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        acc[k] = __fadd_rn(acc[k], __fmul_rn(A.cj[j - 1], win[RA + k + j]));
+#pragma unroll
+                for (int j = R; j >= 1; --j) {
+                    const float4 v = *reinterpret_cast<const float4*>(c - j * SW);
+                    const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        acc[k] = __fadd_rn(acc[k], __fmul_rn(A.cj[j - 1], vv[k]));
+                }
+#pragma unroll
+                for (int j = 1; j <= R; ++j) {
+                    const float4 v = *reinterpret_cast<const float4*>(c + j * SW);
+                    const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        acc[k] = __fadd_rn(acc[k], __fmul_rn(A.cj[j - 1], vv[k]));
+                }
+                // cells outside the global interior keep their slot values;
+                // cells outside the valid region may take any value (never read
+                // by a valid cell), so only the interior test masks stores
+                float* o = out + y * SW + x;
+                if (x >= ix0 && x + 3 < ix1) {
+                    *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (x + k >= ix0 && x + k < ix1) o[k] = acc[k];
+                }
+            }
+        }
         __syncthreads();
     }
     // core of the last two levels (boundary cells carry their slot's values)
