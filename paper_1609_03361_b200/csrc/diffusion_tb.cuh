@@ -78,8 +78,9 @@ __global__ void __launch_bounds__(256) diffusion_tb_kernel(const __grid_constant
     constexpr int SW = L::SW, HA = L::HA;
     extern __shared__ __align__(128) unsigned char smraw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smraw);
-    float* buf[2] = {reinterpret_cast<float*>(smraw + 128),
-                     reinterpret_cast<float*>(smraw + 128) + SW * SW};
+    // buffer b at sbuf + b * SW * SW (pointer arithmetic on the shared
+    // symbol keeps every access an LDS/STS; a pointer array would not)
+    float* const sbuf = reinterpret_cast<float*>(smraw + 128);
     const int tid = threadIdx.x;
     const int tx = tid & 31, ty = tid >> 5;  // 32 x 8 (loads / stores)
     const int T = A.T;
@@ -94,8 +95,8 @@ __global__ void __launch_bounds__(256) diffusion_tb_kernel(const __grid_constant
     if (tid == 0) {
         mbar_arrive_expect_tx(bar, 2 * SW * SW * sizeof(float));
         // buffer b holds the slot of level parity (t0 + b)
-        tma_load_2d(buf[0], (A.t0 & 1) ? &A.src1 : &A.src0, gx0, gy0, bar);
-        tma_load_2d(buf[1], (A.t0 & 1) ? &A.src0 : &A.src1, gx0, gy0, bar);
+        tma_load_2d(sbuf, (A.t0 & 1) ? &A.src1 : &A.src0, gx0, gy0, bar);
+        tma_load_2d(sbuf + SW * SW, (A.t0 & 1) ? &A.src0 : &A.src1, gx0, gy0, bar);
     }
     mbar_wait(bar, 0);
     // Each thread updates 4 consecutive a1 cells per visit: one aligned
@@ -104,8 +105,8 @@ __global__ void __launch_bounds__(256) diffusion_tb_kernel(const __grid_constant
     constexpr int RA = (R + 3) / 4 * 4;
     const int lx = tid & 15, ly = tid >> 4;  // 16 vectors x 16 rows per pass
     for (int st = 1; st <= T; ++st) {
-        const float* in = buf[(st - 1) & 1];
-        float* out = buf[st & 1];
+        const float* in = sbuf + ((st - 1) & 1) * (SW * SW);
+        float* out = sbuf + (st & 1) * (SW * SW);
         // cells still valid after this step (core grown by (T - st) R)
         const int grow = HA - (T - st) * R;
         // global interior in smem coordinates
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(256) diffusion_tb_kernel(const __grid_constant
 #pragma unroll
     for (int lv = 0; lv < 2; ++lv) {
         const int level = A.t0 + T - lv;
-        const float* b = buf[(T - lv) & 1];
+        const float* b = sbuf + ((T - lv) & 1) * (SW * SW);
         float* d = A.dst[level & 1];
         for (int y = HA + ty; y < HA + TILE; y += 8) {
             const int gy = gy0 + y;
