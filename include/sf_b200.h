@@ -185,6 +185,19 @@ int sf_slab_chain_run(sf_plan *const *plans, int nplans, int64_t step_begin, int
 int sf_nccl_unique_id(void *out, int bytes);
 int sf_plan_attach_nccl(sf_plan *plan, const void *id, int nranks, int rank);
 
+/* ---- GPU autotune (Operator::autotune, op.cpp:169-221) -----------------
+ * Times every stencil kernel variant compiled for the plan's order (kernel
+ * family, tile, pipeline depth) on `tune_steps` steps of the resident state,
+ * median of `repeats` runs with the state restored before each, keeps the
+ * fastest and restores the state. kind: 0 per-thread loads, 1 scalar TMA,
+ * 2 vector TMA ring, 3 queue-vector TMA. */
+typedef struct {
+    int kind, tile_nx, tile_ty, vec_warps, stages;
+    float median_ms;
+} sf_tune_entry;
+int sf_plan_autotune(sf_plan *plan, int64_t tune_steps, int repeats, sf_tune_entry *entries,
+                     int max_entries, int *n_entries);
+
 /* Folded diffusion constants (exact rationals -> double -> f32). */
 int sf_diffusion_constants(int order, int64_t alpha_num, int64_t alpha_den, int64_t dx_num,
                            int64_t dx_den, float *c0, int *has_c0, float *cj /* [8] */);

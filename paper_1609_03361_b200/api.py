@@ -280,6 +280,23 @@ class Operator:
         argv, n = self._argv(buffers)
         check(lib.sf_plan_download(self._plan, argv, n))
 
+    KINDS = {0: "per-thread-load", 1: "tma", 2: "vector-tma", 3: "queue-vector-tma"}
+
+    def autotune(self, tune_nt=5, repeats=3):
+        """Operator::autotune (op.cpp:169-221) on the GPU: time every stencil
+        variant on `tune_nt` steps of the uploaded state (restored before each
+        run), keep the fastest. Returns [(description, median_seconds)], best."""
+        ents = (_lib.TuneEntry * 64)()
+        n = C.c_int()
+        check(lib.sf_plan_autotune(self._plan, tune_nt, repeats, ents, 64, C.byref(n)))
+        rep = []
+        for e in ents[: min(n.value, 64)]:
+            desc = (f"{self.KINDS[e.kind]} nx={e.tile_nx} ty={e.tile_ty} warps={e.vec_warps} "
+                    f"stages={e.stages}")
+            rep.append((desc, e.median_ms / 1e3))
+        best = min(rep, key=lambda x: x[1]) if rep else None
+        return rep, best
+
     def time(self, stencil=True):
         """(total_ms, stencil_ms, kernel_launches) of one device-timed run."""
         tot = C.c_float()

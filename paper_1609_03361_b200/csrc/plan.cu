@@ -123,6 +123,7 @@ struct sf_plan {
     bool use_vecq = false; // ... with the a0 neighbours in a register queue (radius >= 5)
     int vec_warps = 8;
     int tma_stages = 4;
+    int stages_override = 0;  // autotune: > 0 forces the pipeline depth
     size_t tma_smem = 0;
     CUtensorMap tm_cur[3], tm_pme[3], tm_m, tm_eta;
     // FWI: history (nt+2 levels), adjoint slots v, gradient
@@ -562,6 +563,7 @@ void setup_tma(Plan& p) {
             const int v = std::atoi(env);
             if (v >= 2 && v <= 16) stages = v;
         }
+        if (p.stages_override >= 2) stages = p.stages_override;
         p.tma_stages = stages;
         p.tma_smem = vecq_smem_bytes(r, p.vec_warps, stages);
         for (int fwd = 0; fwd < 2; ++fwd) {
@@ -579,6 +581,7 @@ void setup_tma(Plan& p) {
             const int v = std::atoi(env);
             if (v >= 2 && v <= 16) stages = v;
         }
+        if (p.stages_override >= 2) stages = p.stages_override;
         p.tma_stages = stages;
         p.tma_smem = vec_smem_bytes(r, p.vec_warps, stages);
         for (int fwd = 0; fwd < 2; ++fwd) {
@@ -603,6 +606,7 @@ void setup_tma(Plan& p) {
         const int v = std::atoi(env);
         if (v >= 2 && v <= 16) stages = v;
     }
+    if (p.stages_override >= 2) stages = p.stages_override;
     p.tma_stages = stages;
     p.tma_smem = tma_smem_bytes(r, nx, stages);
     for (int fwd = 0; fwd < 2; ++fwd) {
@@ -1383,6 +1387,8 @@ void enable_tma(Plan& p) {
     set_grid(p);
 }
 
+
+
 void init_device(Plan& p, int device) {
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
@@ -1590,6 +1596,135 @@ sf_plan::~sf_plan() {
 
 using sfb::guard;
 using sfb::Status;
+
+namespace sfb {
+namespace {
+
+// ---------------------------------------------------------------------------
+// GPU autotune (the reference's Operator::autotune, op.cpp:169-221, searches
+// CPU cache-blocking plans; here the search space is the stencil kernel
+// family, tile shape and pipeline depth).
+struct StencilConfig {
+    int kind;  // 0 per-thread loads, 1 scalar TMA, 2 vector TMA (ring), 3 queue vector TMA
+    int tile_nx, tile_ty, vec_warps, stages;
+};
+
+void drop_graphs(Plan& p) {
+    for (auto& kv : p.graphs) cudaGraphExecDestroy(kv.second);
+    p.graphs.clear();
+}
+
+void apply_config(Plan& p, const StencilConfig& c) {
+    drop_graphs(p);
+    p.use_tma = p.use_vec = p.use_vecq = false;
+    p.tile_nx = c.tile_nx;
+    p.tile_ty = c.tile_ty;
+    p.vec_warps = c.vec_warps;
+    p.stages_override = c.stages;
+    if (c.kind >= 1) {
+        p.use_vec = c.kind >= 2;
+        p.use_vecq = c.kind == 3;
+        setup_tma(p);
+        p.use_tma = true;
+    }
+    set_grid(p);
+}
+
+StencilConfig current_config(const Plan& p) {
+    return {p.use_vecq ? 3 : p.use_vec ? 2 : p.use_tma ? 1 : 0, p.tile_nx, p.tile_ty, p.vec_warps,
+            p.use_tma ? p.tma_stages : 0};
+}
+
+std::vector<StencilConfig> tune_candidates(const Plan& p) {
+    std::vector<StencilConfig> out;
+    const int r = p.ac.radius;
+    for (int nx = 1; nx <= max_tile_nx(r); ++nx)
+        for (int ty : {8, 16}) out.push_back({0, nx, ty, 4, 0});
+    if (r <= 3)
+        for (int nx = 1; nx <= tma_max_nx(r); ++nx)
+            for (int st : {2, 3}) out.push_back({1, nx, 8, 4, st});
+    if (r <= 4)
+        for (int w : {4, 8})
+            for (int st : {2, 3, 4}) out.push_back({2, 2, 2 * w, w, st});
+    if (r >= 5)
+        for (int w : {4, 8})
+            for (int st : {2, 3, 4}) out.push_back({3, 2, 2 * w, w, st});
+    return out;
+}
+
+} // namespace
+} // namespace sfb
+
+
+extern "C" int sf_plan_autotune(sf_plan* p, int64_t tune_steps, int repeats, sf_tune_entry* entries,
+                                int max_entries, int* n_entries) {
+    using namespace sfb;
+    if (!p) return SF_ERR_INVALID;
+    return guard([&] {
+        if (p->kind != sf_plan::ACOUSTIC || p->ndim != 3 || p->slab)
+            throw Status(SF_ERR_INVALID, "autotune tunes single-domain 3D acoustic plans");
+        if (tune_steps < 1 || tune_steps > p->nt) throw Status(SF_ERR_INVALID, "tune_steps range");
+        if (repeats < 1) repeats = 1;
+        SF_CUDA(cudaSetDevice(p->device));
+        // snapshot what a run modifies: the three slots and both series
+        const size_t fbytes = sizeof(float) * (p->slot_elems + field_slack(*p));
+        const size_t sbytes = sizeof(float) * p->nt * p->src.np;
+        const size_t rbytes = sizeof(float) * p->nt * p->rec.np;
+        std::vector<float*> snap;
+        auto copy = [&](void* dst, const void* src, size_t n) {
+            SF_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, p->stream));
+        };
+        for (int s = 0; s < 3; ++s) snap.push_back(dalloc<float>(fbytes / sizeof(float)));
+        snap.push_back(dalloc<float>(std::max<size_t>(sbytes, 4) / sizeof(float)));
+        snap.push_back(dalloc<float>(std::max<size_t>(rbytes, 4) / sizeof(float)));
+        auto restore = [&](bool save) {
+            for (int s = 0; s < 3; ++s)
+                save ? copy(snap[s], p->slot[s], fbytes) : copy(p->slot[s], snap[s], fbytes);
+            save ? copy(snap[3], p->src.series, sbytes) : copy(p->src.series, snap[3], sbytes);
+            save ? copy(snap[4], p->rec.series, rbytes) : copy(p->rec.series, snap[4], rbytes);
+        };
+        restore(true);
+        const StencilConfig original = current_config(*p);
+        StencilConfig best = original;
+        float best_ms = -1.0f;
+        int n = 0;
+        for (const StencilConfig& c : tune_candidates(*p)) {
+            try {
+                apply_config(*p, c);
+            } catch (const Status&) {
+                continue;  // does not fit (shared memory) or not compiled
+            }
+            std::vector<float> t;
+            for (int rep = 0; rep < repeats + 1; ++rep) {  // first run warms the graph
+                restore(false);
+                SF_CUDA(cudaEventRecord(p->ev0, p->stream));
+                run_steps(*p, 0, tune_steps);
+                SF_CUDA(cudaEventRecord(p->ev1, p->stream));
+                check_kernel_errors(*p);
+                float ms = 0;
+                SF_CUDA(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+                if (rep > 0) t.push_back(ms);
+            }
+            std::sort(t.begin(), t.end());
+            const float med = t[t.size() / 2];
+            if (entries && n < max_entries)
+                entries[n] = {c.kind, c.tile_nx, c.tile_ty, c.vec_warps, p->use_tma ? p->tma_stages : 0,
+                              med};
+            ++n;
+            if (best_ms < 0 || med < best_ms) {
+                best_ms = med;
+                best = c;
+            }
+            drop_graphs(*p);
+        }
+        apply_config(*p, best);
+        restore(false);
+        SF_CUDA(cudaStreamSynchronize(p->stream));
+        for (float* f : snap) dfree(f);
+        if (n_entries) *n_entries = n;
+    });
+}
+
 
 extern "C" {
 

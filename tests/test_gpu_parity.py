@@ -307,3 +307,52 @@ def test_diffusion_temporal_blocking_vs_oracle(sf, port, order, n, nt):
     ref = u.copy()
     port.diffusion_run(ref, order, (1, 3), (1, n - 1), nt)
     assert_parity(b.u.data, ref)
+
+
+VARIANTS = [{}, {"SF_VEC": "0"}, {"SF_NO_TMA": "1"}, {"SF_VEC": "0", "SF_TMA": "1"},
+            {"SF_VECQ": "0"}, {"SF_VEC_WARPS": "8"}, {"SF_TMA_STAGES": "2"},
+            {"SF_VEC": "0", "SF_NO_TMA": "1", "SF_TILE": "2,16"}]
+
+
+@pytest.mark.parametrize("order", [2, 6, 8, 12])
+@pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
+def test_every_kernel_variant_bitwise(sf, port, monkeypatch, order, env):
+    """Each stencil kernel family (per-thread loads, scalar TMA, vector TMA
+    ring, queue-vector TMA), tile and pipeline depth reproduces the oracle."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    shape = (29, 37, 101)
+    nt = 9
+    c = random_case(port, shape, order, seed=order + 31)
+    rng = c["rng"]
+    src = rng.standard_normal((nt, 3)).astype(np.float32)
+    rec = np.zeros((nt, 17), np.float32)
+    out = run_plan_raw(sf, shape, order, True, c["dt"], 10.0, nt, c["m"], c["eta"], src.copy(),
+                       c["src_ci"], c["src_w"], rec.copy(), c["rec_ci"], c["rec_w"])
+    coefs = port.coefs(3, order, True, c["dt"], 10.0)
+    u = np.zeros((3,) + shape, np.float32)
+    port.acoustic_run(coefs, u, c["m"], c["eta"], src, c["src_ci"], c["src_w"], rec, c["rec_ci"],
+                      c["rec_w"], nt)
+    assert_parity(out[0], u)
+    assert_parity(out[6], rec)
+
+
+@pytest.mark.parametrize("order", [4, 12])
+def test_autotune_then_parity(sf, port, order):
+    """Operator::autotune on the GPU: every candidate is timed, the best is
+    kept, the state is restored, and the tuned plan still matches the oracle."""
+    model = sf.AcousticModel(shape=(40, 44, 70), nt=12, boundary_width=5, spacing=10.0,
+                             space_order=order)
+    s = sf.acoustic_build(model, True)
+    s.op.upload()
+    report, best = s.op.autotune(tune_nt=4, repeats=1)
+    assert len(report) >= 4 and best is not None
+    assert all(t > 0 for _, t in report)
+    s.op.apply()
+    c = port.coefs(3, order, True, s.dt, 10.0)
+    u = np.zeros_like(s.field.data)
+    rec = np.zeros_like(s.rec.data.data)
+    port.acoustic_run(c, u, s.m.data, s.eta.data, s.src.data.data.copy(), s.src.ci.data,
+                      s.src.w.data, rec, s.rec.ci.data, s.rec.w.data, model.nt)
+    assert_parity(s.field.data, u)
+    assert_parity(s.rec.data.data, rec)
