@@ -185,6 +185,13 @@ int sf_slab_chain_run(sf_plan *const *plans, int nplans, int64_t step_begin, int
 int sf_nccl_unique_id(void *out, int bytes);
 int sf_plan_attach_nccl(sf_plan *plan, const void *id, int nranks, int rank);
 
+/* ---- HBM-resident buffer I/O (save_buffer / load_buffer, grid.cpp:213-254)
+ * Argument `name` (signature name, e.g. "u", "m", "rec") written from / read
+ * into the plan's device mirror in the reference's SFG1 binary format, so
+ * files interchange with the reference's own save_buffer/load_buffer. */
+int sf_plan_save_buffer(sf_plan *plan, const char *name, const char *path);
+int sf_plan_load_buffer(sf_plan *plan, const char *name, const char *path);
+
 /* ---- GPU autotune (Operator::autotune, op.cpp:169-221) -----------------
  * Times every stencil kernel variant compiled for the plan's order (kernel
  * family, tile, pipeline depth) on `tune_steps` steps of the resident state,

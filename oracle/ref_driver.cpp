@@ -250,3 +250,15 @@ int sfref_adjoint_test(int ndim, const long* shape, int boundary_width, double s
     });
 }
 }
+
+extern "C" {
+// save_buffer / load_buffer (grid.cpp:213-254) on a named GridFunction.
+int sfref_save_buffer(void* hp, const char* name, const char* path) {
+    Handle* h = static_cast<Handle*>(hp);
+    return guard([&] { save_buffer(*h->grid->find(name), path); });
+}
+int sfref_load_buffer(void* hp, const char* name, const char* path) {
+    Handle* h = static_cast<Handle*>(hp);
+    return guard([&] { load_buffer(*h->grid->find(name), path); });
+}
+}

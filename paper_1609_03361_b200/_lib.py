@@ -37,7 +37,7 @@ EXPORTS = [
     "sf_interpolation_weights", "sf_stable_dt", "sf_ricker", "sf_build_medium",
     "sf_acoustic_constants", "sf_diffusion_constants",
     "sf_acoustic_plan_create_slab", "sf_slab_chain_run", "sf_nccl_unique_id",
-    "sf_plan_attach_nccl", "sf_plan_autotune",
+    "sf_plan_attach_nccl", "sf_plan_autotune", "sf_plan_save_buffer", "sf_plan_load_buffer",
 ]
 
 
@@ -114,6 +114,8 @@ def _bind(lib):
     lib.sf_slab_chain_run.argtypes = [C.POINTER(_vp), C.c_int, C.c_int64, C.c_int64]
     lib.sf_nccl_unique_id.argtypes = [C.c_char_p, C.c_int]
     lib.sf_plan_attach_nccl.argtypes = [_vp, C.c_char_p, C.c_int, C.c_int]
+    lib.sf_plan_save_buffer.argtypes = [_vp, C.c_char_p, C.c_char_p]
+    lib.sf_plan_load_buffer.argtypes = [_vp, C.c_char_p, C.c_char_p]
     lib.sf_plan_autotune.argtypes = [_vp, C.c_int64, C.c_int, C.POINTER(TuneEntry), C.c_int,
                                      C.POINTER(C.c_int)]
     return lib

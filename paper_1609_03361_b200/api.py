@@ -280,6 +280,14 @@ class Operator:
         argv, n = self._argv(buffers)
         check(lib.sf_plan_download(self._plan, argv, n))
 
+    def save_buffer(self, name, path):
+        """save_buffer (grid.cpp:215-234) straight from the HBM mirror."""
+        check(lib.sf_plan_save_buffer(self._plan, name.encode(), str(path).encode()))
+
+    def load_buffer(self, name, path):
+        """load_buffer (grid.cpp:236-254) straight into the HBM mirror."""
+        check(lib.sf_plan_load_buffer(self._plan, name.encode(), str(path).encode()))
+
     KINDS = {0: "per-thread-load", 1: "tma", 2: "vector-tma", 3: "queue-vector-tma"}
 
     def autotune(self, tune_nt=5, repeats=3):

@@ -1726,6 +1726,133 @@ extern "C" int sf_plan_autotune(sf_plan* p, int64_t tune_steps, int repeats, sf_
 }
 
 
+
+// ---------------------------------------------------------------------------
+// HBM-resident GridFunction I/O in the reference's binary format
+// (save_buffer / load_buffer, grid.cpp:213-254): magic "SFG1" | name |
+// element id (f32 0, f64 1, i32 2) | ndim | extents | raw little-endian data,
+// written straight from (read straight into) the device mirrors.
+namespace sfb {
+namespace {
+
+struct BufferView {
+    std::string name;
+    int elem;                      // 0 f32, 2 i32
+    std::vector<uint32_t> extents;
+};
+
+BufferView buffer_view(const Plan& p, int i) {
+    BufferView v;
+    v.name = p.arg_names.at(i);
+    v.elem = (v.name == "src_ci" || v.name == "rec_ci") ? 2 : 0;
+    auto field = [&](int slots) {
+        if (slots) v.extents.push_back(static_cast<uint32_t>(slots));
+        for (int d = 0; d < p.ndim; ++d) v.extents.push_back(static_cast<uint32_t>(p.n[d]));
+    };
+    const int corners = 1 << p.ndim;
+    if (p.kind == Plan::DIFFUSION) {
+        field(2);
+        return v;
+    }
+    switch (i) {
+        case 0: field(3); break;
+        case 1: case 2: field(0); break;
+        case 3: v.extents = {static_cast<uint32_t>(p.nt), static_cast<uint32_t>(p.src.np)}; break;
+        case 4: v.extents = {static_cast<uint32_t>(p.src.np), static_cast<uint32_t>(p.ndim)}; break;
+        case 5: v.extents = {static_cast<uint32_t>(p.src.np), static_cast<uint32_t>(corners)}; break;
+        case 6: v.extents = {static_cast<uint32_t>(p.nt), static_cast<uint32_t>(p.rec.np)}; break;
+        case 7: v.extents = {static_cast<uint32_t>(p.rec.np), static_cast<uint32_t>(p.ndim)}; break;
+        case 8: v.extents = {static_cast<uint32_t>(p.rec.np), static_cast<uint32_t>(corners)}; break;
+        default: throw Status(SF_ERR_INVALID, "argument index out of range");
+    }
+    return v;
+}
+
+int find_arg(const Plan& p, const char* name) {
+    for (size_t i = 0; i < p.arg_names.size(); ++i)
+        if (p.arg_names[i] == name) return static_cast<int>(i);
+    throw Status(SF_ERR_INVALID, std::string("no buffer named ") + name);
+}
+
+// host staging of argument i through the plan's own download/upload paths
+void transfer_arg(Plan& p, int i, void* host, bool to_host) {
+    std::vector<void*> args(p.arg_names.size(), nullptr);
+    args[i] = host;
+    if (to_host)
+        download_any(p, args.data(), static_cast<int>(args.size()));
+    else
+        upload_any(p, args.data(), static_cast<int>(args.size()));
+    if (!to_host) SF_CUDA(cudaStreamSynchronize(p.stream));
+}
+
+} // namespace
+} // namespace sfb
+
+extern "C" int sf_plan_save_buffer(sf_plan* p, const char* name, const char* path) {
+    using namespace sfb;
+    if (!p || !name || !path) return SF_ERR_INVALID;
+    return guard([&] {
+        if (p->kind == sf_plan::FWI) throw Status(SF_ERR_INVALID, "FWI plans have no buffers");
+        const int i = find_arg(*p, name);
+        const BufferView v = buffer_view(*p, i);
+        std::vector<char> host(static_cast<size_t>(p->arg_bytes.at(i)));
+        // ci / w are not written by the kernels: the device copies are the uploaded ones
+        if (i == 4 || i == 5 || i == 7 || i == 8) {
+            const PointSet& ps = i < 6 ? p->src : p->rec;
+            const void* dev = (i == 4 || i == 7) ? static_cast<const void*>(ps.ci) : ps.w;
+            SF_CUDA(cudaMemcpy(host.data(), dev, host.size(), cudaMemcpyDeviceToHost));
+        } else {
+            transfer_arg(*p, i, host.data(), true);
+        }
+        FILE* f = std::fopen(path, "wb");
+        if (!f) throw Status(SF_ERR_INVALID, std::string("cannot open for write: ") + path);
+        auto put = [&](uint32_t x) { std::fwrite(&x, 4, 1, f); };
+        put(0x53464731u);
+        put(static_cast<uint32_t>(v.name.size()));
+        std::fwrite(v.name.data(), 1, v.name.size(), f);
+        put(static_cast<uint32_t>(v.elem));
+        put(static_cast<uint32_t>(v.extents.size()));
+        for (uint32_t e : v.extents) put(e);
+        const size_t wrote = std::fwrite(host.data(), 1, host.size(), f);
+        std::fclose(f);
+        if (wrote != host.size()) throw Status(SF_ERR_INVALID, std::string("short write: ") + path);
+    });
+}
+
+extern "C" int sf_plan_load_buffer(sf_plan* p, const char* name, const char* path) {
+    using namespace sfb;
+    if (!p || !name || !path) return SF_ERR_INVALID;
+    return guard([&] {
+        if (p->kind == sf_plan::FWI) throw Status(SF_ERR_INVALID, "FWI plans have no buffers");
+        const int i = find_arg(*p, name);
+        const BufferView v = buffer_view(*p, i);
+        FILE* f = std::fopen(path, "rb");
+        if (!f) throw Status(SF_ERR_INVALID, std::string("cannot open for read: ") + path);
+        auto get = [&]() {
+            uint32_t x = 0;
+            if (std::fread(&x, 4, 1, f) != 1) x = 0xFFFFFFFFu;
+            return x;
+        };
+        auto fail = [&](const std::string& m) {
+            std::fclose(f);
+            throw Status(SF_ERR_INVALID, m + " in " + path);
+        };
+        if (get() != 0x53464731u) fail("bad magic");
+        const uint32_t nlen = get();
+        if (nlen > 4096) fail("bad name length");
+        std::string fname(nlen, '\0');
+        if (std::fread(fname.data(), 1, nlen, f) != nlen) fail("short read");
+        if (get() != static_cast<uint32_t>(v.elem)) fail("element type mismatch");
+        if (get() != v.extents.size()) fail("rank mismatch");
+        for (uint32_t e : v.extents)
+            if (get() != e) fail("shape mismatch");
+        std::vector<char> host(static_cast<size_t>(p->arg_bytes.at(i)));
+        if (std::fread(host.data(), 1, host.size(), f) != host.size()) fail("short read");
+        std::fclose(f);
+        transfer_arg(*p, i, host.data(), false);
+    });
+}
+
 extern "C" {
 
 const char* sf_last_error(void) { return sfb::g_error.c_str(); }

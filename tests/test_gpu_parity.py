@@ -356,3 +356,32 @@ def test_autotune_then_parity(sf, port, order):
                       s.src.w.data, rec, s.rec.ci.data, s.rec.w.data, model.nt)
     assert_parity(s.field.data, u)
     assert_parity(s.rec.data.data, rec)
+
+
+def test_hbm_buffer_io_interchanges_with_reference(sf, ref, tmp_path):
+    """save_buffer/load_buffer from HBM in the reference's SFG1 format: files
+    written from the device load into the reference and vice versa."""
+    import ctypes as C
+    from oracle_lib import AcousticCase, ref_acoustic
+    ref.lib.sfref_save_buffer.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p]
+    ref.lib.sfref_load_buffer.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p]
+    model = sf.AcousticModel(shape=(24, 24, 20), nt=12, boundary_width=4)
+    s = sf.acoustic_forward(model)
+    op = ref_acoustic(ref, AcousticCase(shape=(24, 24, 20), nt=12, boundary_width=4), True)
+    for name, dt, shape in [("u", np.float32, (3, 24, 24, 20)), ("rec", np.float32, (12, 8)),
+                            ("src_ci", np.int32, (1, 3)), ("m", np.float32, (24, 24, 20))]:
+        path = str(tmp_path / f"{name}.sfg")
+        s.op.save_buffer(name, path)
+        assert ref.lib.sfref_load_buffer(op.h, name.encode(), path.encode()) == 0, ref.error()
+        want = {"u": s.field.data, "rec": s.rec.data.data, "src_ci": s.src.ci.data,
+                "m": s.m.data}[name]
+        assert np.array_equal(op.get(name, dt, shape), want)
+    # reference -> device
+    op.apply()
+    path = str(tmp_path / "u_ref.sfg")
+    assert ref.lib.sfref_save_buffer(op.h, b"u", path.encode()) == 0
+    s.op.load_buffer("u", path)
+    s.op.download()
+    assert np.array_equal(bits(s.field.data), bits(op.get("u", np.float32, (3, 24, 24, 20))))
+    with pytest.raises(sf.SfError):
+        s.op.load_buffer("m", path)  # shape/rank mismatch is rejected
