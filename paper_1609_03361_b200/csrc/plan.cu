@@ -77,6 +77,7 @@ struct PointSet {
     float* w = nullptr;       // [np][2^ndim]
     // injection CSR over distinct target cells
     int ncells = 0;
+    int nband0 = 0;  // slabs: the first nband0 cells lie in the boundary bands
     int64_t* cell_off = nullptr;
     int* start = nullptr;
     int* cp = nullptr;
@@ -145,6 +146,17 @@ struct sf_plan {
     void* nccl_comm = nullptr;
     int nccl_rank = -1, nccl_nranks = 0;
     cudaEvent_t ev_copy = nullptr;  // in-process chain: halo copies issued
+    // overlap of the halo exchange with the inner planes (slabs, owned >= 2r)
+    struct ZRange {
+        int z0 = 0, z1 = 0;
+        dim3 grid;
+        int zchunk = 0;
+    };
+    bool overlap = false;
+    bool overlap_disabled = false;
+    ZRange zr_lo, zr_hi, zr_in;
+    cudaStream_t comm = nullptr;
+    cudaEvent_t ev_band = nullptr, ev_comm = nullptr;
 
     ~sf_plan();
 };
@@ -248,6 +260,13 @@ void upload_points(Plan& p, PointSet& s, const float* series, const int* ci, con
         int64_t off;
         int p;
         float w;
+        int band;  // 0: a slab's boundary band (sent to a neighbour), 1: inner
+    };
+    const int r = p.ac.radius;
+    auto band_of = [&](int c0) {
+        if (p.slab && ((p.has_lower && c0 < p.own_lo + r) || (p.has_upper && c0 >= p.own_hi - r)))
+            return 0;
+        return p.slab ? 1 : 0;
     };
     std::vector<Contrib> cs;
     cs.reserve(static_cast<size_t>(s.np * corners));
@@ -257,18 +276,21 @@ void upload_points(Plan& p, PointSet& s, const float* series, const int* ci, con
             for (int d = 0; d < p.ndim; ++d) c[d] = s.host_ci[q * p.ndim + d] + ((k >> d) & 1);
             // a slab applies only the corners it owns; neighbours apply theirs
             if (c[0] < p.own_lo || c[0] >= p.own_hi) continue;
-            cs.push_back({device_offset(p, c), static_cast<int>(q), w[q * corners + k]});
+            cs.push_back({device_offset(p, c), static_cast<int>(q), w[q * corners + k], band_of(c[0])});
         }
-    // stable sort by cell keeps ascending p within a cell
-    std::stable_sort(cs.begin(), cs.end(),
-                     [](const Contrib& a, const Contrib& b) { return a.off < b.off; });
+    // stable sort by (band, cell) keeps ascending p within a cell
+    std::stable_sort(cs.begin(), cs.end(), [](const Contrib& a, const Contrib& b) {
+        return a.band != b.band ? a.band < b.band : a.off < b.off;
+    });
     std::vector<int64_t> cells;
     std::vector<int> start, cp;
     std::vector<float> cw;
+    int nband0 = 0;
     for (size_t i = 0; i < cs.size(); ++i) {
         if (i == 0 || cs[i].off != cs[i - 1].off) {
             cells.push_back(cs[i].off);
             start.push_back(static_cast<int>(i));
+            if (cs[i].band == 0) ++nband0;
         }
         cp.push_back(cs[i].p);
         cw.push_back(cs[i].w);
@@ -285,6 +307,7 @@ void upload_points(Plan& p, PointSet& s, const float* series, const int* ci, con
     dfree(s.cp);
     dfree(s.cw);
     s.ncells = cs.empty() ? 0 : static_cast<int>(cells.size());
+    s.nband0 = cs.empty() ? 0 : nband0;
     s.cell_off = dalloc<int64_t>(cells.size());
     s.start = dalloc<int>(start.size());
     s.cp = dalloc<int>(cp.size());
@@ -727,7 +750,10 @@ bool map_for(const Plan& p, const float* f, MapSel* m) {
 }
 
 void launch_stencil(const Plan& p, float* out, const float* cur, const float* prev,
-                    float* grad = nullptr, const float* uhist = nullptr) {
+                    float* grad = nullptr, const float* uhist = nullptr,
+                    const sf_plan::ZRange* zr = nullptr) {
+    if (zr && zr->z0 >= zr->z1) return;
+    const dim3 grid3 = zr ? zr->grid : p.grid3;
     MapSel mc, mp, mo, mu;
     const bool maps = p.use_tma && p.ndim == 3 && map_for(p, cur, &mc) && map_for(p, prev, &mp);
     const bool grad_ok =
@@ -749,9 +775,9 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
         T.n0 = static_cast<int>(p.n[0]);
         T.n1 = static_cast<int>(p.n[1]);
         T.n2 = static_cast<int>(p.n[2]);
-        T.zchunk = p.zchunk;
-        T.z0 = p.z0;
-        T.z1 = p.z1;
+        T.zchunk = zr ? zr->zchunk : p.zchunk;
+        T.z0 = zr ? zr->z0 : p.z0;
+        T.z1 = zr ? zr->z1 : p.z1;
         T.stages = p.tma_stages;
         T.ce = p.ac.ce;
         T.cm = p.ac.cm;
@@ -770,35 +796,40 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
         }
         if (p.use_vecq) {
             if (p.ac.forward)
-                launch_vecq<true>(p.ac.radius, p.vec_warps, p.grid3, p.tma_smem, p.stream, T);
+                launch_vecq<true>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T);
             else
-                launch_vecq<false>(p.ac.radius, p.vec_warps, p.grid3, p.tma_smem, p.stream, T);
+                launch_vecq<false>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T);
             return;
         }
         if (p.use_vec) {
             if (p.ac.forward)
-                launch_vec<true>(p.ac.radius, p.vec_warps, p.grid3, p.tma_smem, p.stream, T);
+                launch_vec<true>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T);
             else
-                launch_vec<false>(p.ac.radius, p.vec_warps, p.grid3, p.tma_smem, p.stream, T);
+                launch_vec<false>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T);
             return;
         }
         if (p.ac.forward)
-            launch_tma<true>(p.ac.radius, p.tile_nx, p.grid3, p.tma_smem, p.stream, T);
+            launch_tma<true>(p.ac.radius, p.tile_nx, grid3, p.tma_smem, p.stream, T);
         else
-            launch_tma<false>(p.ac.radius, p.tile_nx, p.grid3, p.tma_smem, p.stream, T);
+            launch_tma<false>(p.ac.radius, p.tile_nx, grid3, p.tma_smem, p.stream, T);
         return;
     }
     StencilArgs A = stencil_args(p, out, cur, prev);
     A.grad = grad;
     A.uhist = uhist;
+    if (zr) {
+        A.z0 = zr->z0;
+        A.z1 = zr->z1;
+        A.zchunk = zr->zchunk;
+    }
     const int r = p.ac.radius;
     if (p.ndim == 3) {
         if (grad) {
-            launch_acoustic3d_r<false, true>(r, p.tile_nx, p.tile_ty, p.grid3, p.stream, A);
+            launch_acoustic3d_r<false, true>(r, p.tile_nx, p.tile_ty, grid3, p.stream, A);
         } else if (p.ac.forward) {
-            launch_acoustic3d_r<true, false>(r, p.tile_nx, p.tile_ty, p.grid3, p.stream, A);
+            launch_acoustic3d_r<true, false>(r, p.tile_nx, p.tile_ty, grid3, p.stream, A);
         } else {
-            launch_acoustic3d_r<false, false>(r, p.tile_nx, p.tile_ty, p.grid3, p.stream, A);
+            launch_acoustic3d_r<false, false>(r, p.tile_nx, p.tile_ty, grid3, p.stream, A);
         }
     } else {
         dim3 b(64, 4);
@@ -810,8 +841,10 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
     }
 }
 
-void launch_inject(const Plan& p, const PointSet& s, float* field, int64_t row) {
-    if (s.ncells == 0 || s.np == 0) return;
+void launch_inject(const Plan& p, const PointSet& s, float* field, int64_t row, int first = 0,
+                   int count = -1) {
+    if (count < 0) count = s.ncells - first;
+    if (count <= 0 || s.np == 0) return;
     InjectArgs A{};
     A.field = field;
     A.m = p.m;
@@ -821,8 +854,10 @@ void launch_inject(const Plan& p, const PointSet& s, float* field, int64_t row) 
     A.cp = s.cp;
     A.cw = s.cw;
     A.scale = p.ac.src_scale;
-    A.ncells = s.ncells;
-    inject_kernel<<<(s.ncells + 255) / 256, 256, 0, p.stream>>>(A);
+    A.cell_off = s.cell_off + first;
+    A.start = s.start + first;
+    A.ncells = count;
+    inject_kernel<<<(count + 255) / 256, 256, 0, p.stream>>>(A);
 }
 
 void launch_sample(const Plan& p, const PointSet& s, const float* field, int64_t row) {
@@ -954,6 +989,7 @@ void launch_inject_sample(const Plan& p, const PointSet& inj, const PointSet& sm
 
 int64_t launches_per_step_of(const Plan& p) {
     if (p.kind == Plan::DIFFUSION) return 1;  // per step without temporal blocking
+    if (p.nccl_comm && p.overlap) return 6;  // 3 stencil ranges, 2 injections, sampling
     if (p.nccl_comm && (p.has_lower || p.has_upper)) return 3;
     const PointSet& inj = p.ac.forward ? p.src : p.rec;
     const PointSet& smp = p.ac.forward ? p.rec : p.src;
@@ -982,6 +1018,32 @@ void enqueue_acoustic_step(Plan& p, int64_t k, float* const* u, bool stencil_onl
     const StepSlots st = step_slots(p, k, u);
     const PointSet& inj = p.ac.forward ? p.src : p.rec;
     const PointSet& smp = p.ac.forward ? p.rec : p.src;
+    if (p.nccl_comm && p.overlap && !stencil_only) {
+        // boundary bands + their injection -> exchange on the comm stream
+        // while the inner planes are updated and injected
+        launch_stencil(p, st.out, st.cur, st.prev, nullptr, nullptr, &p.zr_lo);
+        launch_stencil(p, st.out, st.cur, st.prev, nullptr, nullptr, &p.zr_hi);
+        launch_inject(p, inj, st.out, st.row, 0, inj.nband0);
+        SF_CUDA(cudaEventRecord(p.ev_band, p.stream));
+        SF_CUDA(cudaStreamWaitEvent(p.comm, p.ev_band, 0));
+        {
+            Plan& q = p;
+            std::swap(q.stream, q.comm);  // exchange enqueued on the comm stream
+            try {
+                launch_exchange_nccl(q, st.out);
+            } catch (...) {
+                std::swap(q.stream, q.comm);
+                throw;
+            }
+            std::swap(q.stream, q.comm);
+        }
+        SF_CUDA(cudaEventRecord(p.ev_comm, p.comm));
+        launch_stencil(p, st.out, st.cur, st.prev, nullptr, nullptr, &p.zr_in);
+        launch_inject(p, inj, st.out, st.row, inj.nband0, inj.ncells - inj.nband0);
+        SF_CUDA(cudaStreamWaitEvent(p.stream, p.ev_comm, 0));
+        launch_sample(p, smp, st.out, st.row);
+        return;
+    }
     launch_stencil(p, st.out, st.cur, st.prev);
     if (stencil_only) return;
     if (p.nccl_comm && (p.has_lower || p.has_upper)) {
@@ -1008,8 +1070,15 @@ void chain_step(sf_plan* const* P, int n, int64_t k) {
             if (i + 1 < n) SF_CUDA(cudaStreamWaitEvent(p.stream, P[i + 1]->ev_copy, 0));
         }
         const StepSlots st = step_slots(p, k, p.slot);
-        launch_stencil(p, st.out, st.cur, st.prev);
-        launch_inject(p, p.ac.forward ? p.src : p.rec, st.out, st.row);
+        const PointSet& inj = p.ac.forward ? p.src : p.rec;
+        if (p.overlap) {  // same split as the NCCL path: bands, copies, then inner planes
+            launch_stencil(p, st.out, st.cur, st.prev, nullptr, nullptr, &p.zr_lo);
+            launch_stencil(p, st.out, st.cur, st.prev, nullptr, nullptr, &p.zr_hi);
+            launch_inject(p, inj, st.out, st.row, 0, inj.nband0);
+        } else {
+            launch_stencil(p, st.out, st.cur, st.prev);
+            launch_inject(p, inj, st.out, st.row);
+        }
         const size_t bytes = static_cast<size_t>(r) * p.plane * sizeof(float);
         if (i > 0) {
             Plan& q = *P[i - 1];
@@ -1027,6 +1096,10 @@ void chain_step(sf_plan* const* P, int n, int64_t k) {
                                         p.device, bytes, p.stream));
         }
         SF_CUDA(cudaEventRecord(p.ev_copy, p.stream));
+        if (p.overlap) {
+            launch_stencil(p, st.out, st.cur, st.prev, nullptr, nullptr, &p.zr_in);
+            launch_inject(p, inj, st.out, st.row, inj.nband0, inj.ncells - inj.nband0);
+        }
     }
     for (int i = 0; i < n; ++i) {
         Plan& p = *P[i];
@@ -1251,10 +1324,12 @@ int max_tile_nx(int r) { return r <= 4 ? 4 : 2; }
 // queue warm-up, so minimise waves(gz) * (chunk(gz) + 2R) over the chunkings
 // that put at least one full wave on the machine.
 // Chunking cost model for one kernel shape (tile wx x wy, resident CTAs/SM).
-void chunk_grid(const Plan& p, int64_t wx, int64_t wy, int per_sm, dim3* grid, int* zchunk) {
+void chunk_grid(const Plan& p, int64_t wx, int64_t wy, int per_sm, dim3* grid, int* zchunk,
+                int64_t nz = -1) {
     const int r = p.ac.radius;
     const int64_t gx = (p.n[2] + wx - 1) / wx, gy = (p.n[1] + wy - 1) / wy;
-    const int64_t nz = p.z1 - p.z0;
+    if (nz < 0) nz = p.z1 - p.z0;
+    if (nz < 1) nz = 1;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
     if (per_sm < 1) per_sm = 1;
@@ -1302,6 +1377,24 @@ void set_grid(Plan& p) {
     }
     p.resident = per_sm;
     chunk_grid(p, wx, wy, per_sm, &p.grid3, &p.zchunk);
+    if (p.slab) {
+        // exchange overlap: boundary bands first, inner planes while the
+        // halos are in flight (needs at least 2r owned interior planes)
+        const int own0 = std::max(p.own_lo, p.z0), own1 = std::min(p.own_hi, p.z1);
+        p.overlap = !p.overlap_disabled && (p.has_lower || p.has_upper) && own1 - own0 >= 2 * r + 1;
+        if (p.overlap) {
+            auto setr = [&](sf_plan::ZRange& z, int a, int b) {
+                z.z0 = a;
+                z.z1 = b;
+                if (b > a) chunk_grid(p, wx, wy, per_sm, &z.grid, &z.zchunk, b - a);
+            };
+            const int lo_end = p.has_lower ? own0 + r : own0;
+            const int hi_beg = p.has_upper ? own1 - r : own1;
+            setr(p.zr_lo, own0, lo_end);
+            setr(p.zr_hi, hi_beg, own1);
+            setr(p.zr_in, lo_end, hi_beg);
+        }
+    }
     if (p.kind == Plan::FWI && p.use_vec && !p.use_vecq) {
         int g = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g, vec_grad_ptr(r), 160, p.smem_grad);
@@ -1585,6 +1678,9 @@ sf_plan::~sf_plan() {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (ev_copy) cudaEventDestroy(ev_copy);
+    if (ev_band) cudaEventDestroy(ev_band);
+    if (ev_comm) cudaEventDestroy(ev_comm);
+    if (comm) cudaStreamDestroy(comm);
     if (nccl_comm) {
         try {
             sfb::nccl().CommDestroy(nccl_comm);
@@ -1947,6 +2043,10 @@ int sf_acoustic_plan_create_slab(const sf_acoustic_desc* d, const sf_slab_desc* 
         p->z0 = static_cast<int>(std::max<int64_t>(sl->own_begin, r) - sl->plane0);
         p->z1 = static_cast<int>(std::min<int64_t>(sl->own_end, sl->global_n0 - r) - sl->plane0);
         SF_CUDA(cudaEventCreateWithFlags(&p->ev_copy, cudaEventDisableTiming));
+        SF_CUDA(cudaEventCreateWithFlags(&p->ev_band, cudaEventDisableTiming));
+        SF_CUDA(cudaEventCreateWithFlags(&p->ev_comm, cudaEventDisableTiming));
+        SF_CUDA(cudaStreamCreateWithFlags(&p->comm, cudaStreamNonBlocking));
+        if (const char* env = std::getenv("SF_NO_OVERLAP")) p->overlap_disabled = env[0] == '1';
         sfb::choose_geometry(*p);
         sfb::enable_tma(*p);
         SF_CUDA(cudaStreamSynchronize(p->stream));
