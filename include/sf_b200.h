@@ -83,6 +83,14 @@ int sf_device_count(void);
 int sf_acoustic_plan_create(const sf_acoustic_desc *desc, int device, sf_plan **out);
 int sf_diffusion_plan_create(const sf_diffusion_desc *desc, int device, sf_plan **out);
 void sf_plan_destroy(sf_plan *plan);
+/* Same plans with the folded constants supplied by the caller instead of
+ * derived from dt/spacing/alpha: the layout of sf_acoustic_constants /
+ * sf_diffusion_constants. Used by the C-source front end (sf-cuda-cc), which
+ * lifts the literals from the reference's generated kernel. */
+int sf_acoustic_plan_create_ex(const sf_acoustic_desc *desc, const float *constants /* [15] */,
+                               const int *time_sel /* [3] */, int device, sf_plan **out);
+int sf_diffusion_plan_create_ex(const sf_diffusion_desc *desc, float c0, int has_c0,
+                                const float *cj /* [8] */, int device, sf_plan **out);
 
 /* Number of buffers the entry takes and their names in declaration order
  * (KernelSignature, codegen.hpp:21-29). */

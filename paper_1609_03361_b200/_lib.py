@@ -29,6 +29,7 @@ SF_ERR_OOM = 7
 EXPORTS = [
     "sf_last_error", "sf_device_count",
     "sf_acoustic_plan_create", "sf_diffusion_plan_create", "sf_plan_destroy",
+    "sf_acoustic_plan_create_ex", "sf_diffusion_plan_create_ex",
     "sf_plan_num_args", "sf_plan_arg_name", "sf_plan_arg_bytes",
     "sf_acoustic_apply", "sf_diffusion_apply", "sf_plan_invoke",
     "sf_plan_upload", "sf_plan_run", "sf_plan_download", "sf_plan_synchronize",
@@ -107,6 +108,10 @@ def _bind(lib):
                                     _vp, C.c_double, _f32p, _f32p]
     lib.sf_acoustic_constants.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                           _f32p, _i32p]
+    lib.sf_acoustic_plan_create_ex.argtypes = [C.POINTER(AcousticDesc), _f32p, _i32p, C.c_int,
+                                               C.POINTER(_vp)]
+    lib.sf_diffusion_plan_create_ex.argtypes = [C.POINTER(DiffusionDesc), C.c_float, C.c_int,
+                                                _f32p, C.c_int, C.POINTER(_vp)]
     lib.sf_diffusion_constants.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                            C.POINTER(C.c_float), C.POINTER(C.c_int), _f32p]
     lib.sf_acoustic_plan_create_slab.argtypes = [C.POINTER(AcousticDesc), C.POINTER(SlabDesc),

@@ -2014,6 +2014,48 @@ int sf_diffusion_plan_create(const sf_diffusion_desc* d, int device, sf_plan** o
 
 void sf_plan_destroy(sf_plan* p) { delete p; }
 
+// Plans whose folded constants come from elsewhere (the C-source front end
+// sf-cuda-cc lifts them from the reference's generated kernel): same layout
+// as sf_acoustic_constants' output.
+int sf_acoustic_plan_create_ex(const sf_acoustic_desc* d, const float* c, const int* tsel,
+                               int device, sf_plan** out) {
+    if (!c || !tsel) return SF_ERR_INVALID;
+    int rc = sf_acoustic_plan_create(d, device, out);
+    if (rc != SF_OK) return rc;
+    sf_plan* p = *out;
+    rc = guard([&] {
+        const bool fwd = d->forward != 0;
+        const int want[3] = {0, fwd ? 2 : 3, fwd ? 3 : 2};
+        for (int k = 0; k < 3; ++k)
+            if (tsel[k] != want[k])
+                throw Status(SF_ERR_INVALID, "time terms are not in the emitted order");
+        p->ac.ce = c[0];
+        p->ac.cm = c[1];
+        for (int k = 0; k < 3; ++k) p->ac.tc[k] = c[2 + k];
+        p->ac.c0 = c[5];
+        for (int j = 0; j < 8; ++j) p->ac.cj[j] = j < p->ac.radius ? c[6 + j] : 0.0f;
+        p->ac.src_scale = c[14];
+        for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+        p->graphs.clear();
+    });
+    if (rc != SF_OK) {
+        delete p;
+        *out = nullptr;
+    }
+    return rc;
+}
+
+int sf_diffusion_plan_create_ex(const sf_diffusion_desc* d, float c0, int has_c0, const float* cj,
+                                int device, sf_plan** out) {
+    if (!cj) return SF_ERR_INVALID;
+    int rc = sf_diffusion_plan_create(d, device, out);
+    if (rc != SF_OK) return rc;
+    (*out)->dc.c0 = c0;
+    (*out)->dc.has_c0 = has_c0 != 0;
+    for (int j = 0; j < 8; ++j) (*out)->dc.cj[j] = j < (*out)->dc.radius ? cj[j] : 0.0f;
+    return SF_OK;
+}
+
 int sf_acoustic_plan_create_slab(const sf_acoustic_desc* d, const sf_slab_desc* sl, int device,
                                  sf_plan** out) {
     if (!out || !d || !sl) return SF_ERR_INVALID;

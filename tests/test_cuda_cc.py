@@ -1,0 +1,207 @@
+"""sf-cuda-cc: the reference's own Operator pipeline compiled onto the B200.
+
+The reference JIT-compiles every operator through $STENCILFORGE_CC
+(jit.cpp:84-95). These tests build operators with the unmodified reference
+(oracle/_ref/libsf_ref.so), once with its default gcc toolchain and once with
+STENCILFORGE_CC=bin/sf-cuda-cc, and require the two runs to leave bitwise
+identical buffers. The CPU tests check the source front end: every lifted
+literal equals the library's own folded constant, and both back ends build.
+"""
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle_lib import AcousticCase, have_ref, ref_acoustic, ref_diffusion
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOOL = os.path.join(ROOT, "bin", "sf-cuda-cc")
+
+needs_ref = pytest.mark.skipif(not have_ref(), reason="reference not built (oracle/_ref)")
+
+ACOUSTIC = [(shape, order, fwd)
+            for shape in ((40, 36), (26, 24, 22))
+            for order in (2, 4, 8, 16)
+            for fwd in (True, False)]
+DIFFUSION = [2, 4, 8, 16]
+
+
+def _case(shape, order, nt=9):
+    ndim = len(shape)
+    return AcousticCase(shape=shape, boundary_width=4, nt=nt, spacing=12.0, space_order=order,
+                        src_coords=[[130.0 + 3 * k] * ndim for k in range(2)],
+                        rec_coords=[[40.0 + 17.5 * i, 200.0 - 9 * i, 55.0][:ndim]
+                                    for i in range(5)])
+
+
+def _buffers(op, names):
+    out = {}
+    for name in names:
+        n = op.ref.lib.sfref_buffer_bytes(op.h, name.encode())
+        dt = np.int32 if name.endswith("_ci") else np.float32
+        out[name] = op.get(name, dt, (n // 4,))
+    return out
+
+
+ACOUSTIC_ARGS = ["m", "eta", "src", "src_ci", "src_w", "rec", "rec_ci", "rec_w"]
+
+
+@needs_ref
+@pytest.mark.parametrize("shape,order,fwd", ACOUSTIC)
+def test_lifted_acoustic_constants_match_library(ref, shape, order, fwd):
+    from paper_1609_03361_b200 import cuda_cc
+    from paper_1609_03361_b200._lib import lib
+    op = ref_acoustic(ref, _case(shape, order), fwd)
+    prog = cuda_cc.parse(op.source())
+    got = cuda_cc.recognise(prog)
+    assert isinstance(got, cuda_cc.AcousticOp)
+    assert got.shape == tuple(shape) and got.order == order and got.forward == fwd
+    assert (got.n_src, got.n_rec, got.nt) == (2, 5, 9)
+    want = np.zeros(15, np.float32)
+    sel = np.zeros(3, np.int32)
+    assert lib.sf_acoustic_constants(len(shape), order, int(fwd), op.dt, 12.0,
+                                     want, sel) == 0
+    assert np.array_equal(np.asarray(got.constants, np.float32).view(np.uint32),
+                          want.view(np.uint32))
+    assert list(sel) == got.tsel
+
+
+@needs_ref
+@pytest.mark.parametrize("order", DIFFUSION)
+def test_lifted_diffusion_constants_match_library(ref, order):
+    from paper_1609_03361_b200 import cuda_cc
+    from paper_1609_03361_b200._lib import lib
+    op = ref_diffusion(ref, 50, 40, (1, 2), (1, 10), 5, order)
+    got = cuda_cc.recognise(cuda_cc.parse(op.source()))
+    assert isinstance(got, cuda_cc.DiffusionOp)
+    c0, has = C.c_float(), C.c_int()
+    cj = np.zeros(8, np.float32)
+    assert lib.sf_diffusion_constants(order, 1, 2, 1, 10, C.byref(c0), C.byref(has),
+                                      cj) == 0
+    assert bool(has.value) == got.has_c0
+    if got.has_c0:
+        assert np.float32(c0.value) == np.float32(got.c0)
+    assert np.array_equal(np.asarray(got.cj, np.float32), cj)
+
+
+def test_unrecognised_source_falls_back_to_generic():
+    from paper_1609_03361_b200 import cuda_cc
+    src = """#include <math.h>
+
+int Operator(float *a_vec, float *b_vec)
+{
+  float (*a)[10] = (float (*)[10]) a_vec;
+  float *b = b_vec;
+  {
+    #pragma omp parallel
+    {
+      #pragma omp for schedule(static)
+      for (int i1 = 0; i1 < 6; i1 += 1)
+      {
+        #pragma omp simd aligned(a:64)
+        for (int i2 = 1; i2 < 9; i2 += 1)
+        {
+          a[i1][i2] = 5.0e-1F*a[i1][i2 - 1] + b[i2];
+        }
+      }
+    }
+  }
+  return 0;
+}
+"""
+    kind, text, lang = cuda_cc.translate(src)
+    assert kind == "generic" and lang == "cuda"
+    assert "__global__ void sfk0" in text and "a[i1][i2] = 5.0e-1F*a[i1][i2 - 1] + b[i2];" in text
+
+
+@needs_ref
+@pytest.mark.parametrize("generic", [False, True])
+def test_tool_builds_shared_library(ref, tmp_path, generic):
+    op = ref_acoustic(ref, _case((26, 24, 22), 8), True)
+    src = tmp_path / "kernel.c"
+    src.write_text(op.source())
+    lib = tmp_path / "kernel.so"
+    env = dict(os.environ)
+    if generic:
+        env["SF_CUDA_CC_GENERIC"] = "1"
+    # the exact command line jit.cpp:67-80 issues
+    cmd = [TOOL, "-std=c99", "-O3", "-march=native", "-fPIC", "-shared", "-ffp-contract=off",
+           "-fopenmp", "-o", str(lib), str(src), "-lm"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    syms = subprocess.run(["nm", "-D", "--defined-only", str(lib)], capture_output=True,
+                          text=True).stdout
+    assert " T Operator" in syms
+
+
+def test_tool_rejects_bad_command_line(tmp_path):
+    r = subprocess.run([TOOL, "-O3"], capture_output=True, text=True)
+    assert r.returncode == 2
+
+
+# ---------------------------------------------------------------------------
+# the reference's pipeline end to end on the GPU
+
+
+@pytest.fixture(scope="module")
+def sf():
+    import paper_1609_03361_b200 as sf
+    if sf._lib.lib.sf_device_count() < 1:
+        pytest.fail("no CUDA device: the GPU tests need a B200")
+    return sf
+
+
+@pytest.fixture
+def cuda_cc_env(monkeypatch):
+    def use(generic):
+        monkeypatch.setenv("STENCILFORGE_CC", TOOL)
+        if generic:
+            monkeypatch.setenv("SF_CUDA_CC_GENERIC", "1")
+        else:
+            monkeypatch.delenv("SF_CUDA_CC_GENERIC", raising=False)
+    return use
+
+
+def _run_acoustic(ref, shape, order, fwd, seed):
+    op = ref_acoustic(ref, _case(shape, order), fwd)
+    rng = np.random.default_rng(seed)
+    field = "u" if fwd else "v"
+    if not fwd:
+        rec = _buffers(op, ["rec"])["rec"]
+        op.set("rec", rng.standard_normal(rec.shape).astype(np.float32))
+    # a non-zero start state exercises every slot of the time buffer
+    n = op.ref.lib.sfref_buffer_bytes(op.h, field.encode()) // 4
+    op.set(field, (1e-3 * rng.standard_normal(n)).astype(np.float32))
+    op.apply()
+    return _buffers(op, [field] + ACOUSTIC_ARGS)
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("shape,order,fwd", ACOUSTIC)
+def test_reference_pipeline_on_gpu_acoustic(sf, ref, cuda_cc_env, shape, order, fwd, generic):
+    want = _run_acoustic(ref, shape, order, fwd, 7)          # reference, gcc
+    cuda_cc_env(generic)
+    got = _run_acoustic(ref, shape, order, fwd, 7)           # reference, sf-cuda-cc
+    for name in want:
+        assert np.array_equal(got[name].view(np.uint32), want[name].view(np.uint32)), name
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("order", DIFFUSION)
+def test_reference_pipeline_on_gpu_diffusion(sf, ref, cuda_cc_env, order, generic):
+    def run():
+        op = ref_diffusion(ref, 70, 66, (1, 2), (1, 10), 23, order)
+        rng = np.random.default_rng(order)
+        op.set("u", rng.random(2 * 70 * 66).astype(np.float32))
+        op.apply()
+        return op.get("u", np.float32, (2, 70, 66))
+    want = run()
+    cuda_cc_env(generic)
+    got = run()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
