@@ -680,10 +680,10 @@ def row_bytes(prog: Program, ctype: str, name: str) -> int:
 # ---------------------------------------------------------------------------
 # driver
 
-def translate(src: str):
+def translate(src: str, generic: bool = False):
     """(kind, source_text, language) for the generated C translation unit."""
     prog = parse(src)
-    op = None if os.environ.get("SF_CUDA_CC_GENERIC") else recognise(prog)
+    op = None if generic else recognise(prog)
     if isinstance(op, AcousticOp):
         return "acoustic", emit_acoustic(op, prog.entry), "c++"
     if isinstance(op, DiffusionOp):
@@ -691,10 +691,10 @@ def translate(src: str):
     return "generic", emit_generic(prog), "cuda"
 
 
-def build(src_path: str, out_path: str) -> str:
+def build(src_path: str, out_path: str, generic: bool = False) -> str:
     with open(src_path) as f:
         src = f.read()
-    kind, text, lang = translate(src)
+    kind, text, lang = translate(src, generic)
     lib_dir = HERE
     inc = os.path.join(ROOT, "include")
     with tempfile.TemporaryDirectory() as td:
@@ -718,7 +718,7 @@ def build(src_path: str, out_path: str) -> str:
     return kind
 
 
-def main(argv=None):
+def main(argv=None, generic=False):
     """gcc-compatible command line: `... -o lib.so src.c [flags]` (jit.cpp:67-80)."""
     argv = list(sys.argv[1:] if argv is None else argv)
     out = None
@@ -737,12 +737,15 @@ def main(argv=None):
         sys.stderr.write("sf-cuda-cc: need exactly one source and -o <lib>\n")
         return 2
     try:
-        kind = build(srcs[0], out)
+        kind = build(srcs[0], out, generic or bool(os.environ.get("SF_CUDA_CC_GENERIC")))
     except Unsupported as e:
         sys.stderr.write(f"sf-cuda-cc: unsupported generated code: {e}\n")
         return 1
     if os.environ.get("SF_CUDA_CC_VERBOSE"):
         sys.stderr.write(f"sf-cuda-cc: {srcs[0]} -> {out} ({kind})\n")
+    if os.environ.get("SF_CUDA_CC_LOG"):
+        with open(os.environ["SF_CUDA_CC_LOG"], "a") as f:
+            f.write(f"{kind} {out}\n")
     return 0
 
 

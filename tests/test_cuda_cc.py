@@ -123,17 +123,16 @@ def test_tool_builds_shared_library(ref, tmp_path, generic):
     src = tmp_path / "kernel.c"
     src.write_text(op.source())
     lib = tmp_path / "kernel.so"
-    env = dict(os.environ)
-    if generic:
-        env["SF_CUDA_CC_GENERIC"] = "1"
+    env = dict(os.environ, SF_CUDA_CC_LOG=str(tmp_path / "log"))
     # the exact command line jit.cpp:67-80 issues
-    cmd = [TOOL, "-std=c99", "-O3", "-march=native", "-fPIC", "-shared", "-ffp-contract=off",
+    cmd = [TOOL + ("-generic" if generic else ""), "-std=c99", "-O3", "-march=native", "-fPIC", "-shared", "-ffp-contract=off",
            "-fopenmp", "-o", str(lib), str(src), "-lm"]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     syms = subprocess.run(["nm", "-D", "--defined-only", str(lib)], capture_output=True,
                           text=True).stdout
     assert " T Operator" in syms
+    assert (tmp_path / "log").read_text().split()[0] == ("generic" if generic else "acoustic")
 
 
 def test_tool_rejects_bad_command_line(tmp_path):
@@ -154,13 +153,16 @@ def sf():
 
 
 @pytest.fixture
-def cuda_cc_env(monkeypatch):
+def cuda_cc_env(monkeypatch, tmp_path):
+    """Point the reference at sf-cuda-cc (the generic flavour is a separate
+    executable so the reference's JIT cache, keyed on the executable, keeps
+    the two builds apart) and return the tool's build log."""
+    log = tmp_path / "sf-cuda-cc.log"
+
     def use(generic):
-        monkeypatch.setenv("STENCILFORGE_CC", TOOL)
-        if generic:
-            monkeypatch.setenv("SF_CUDA_CC_GENERIC", "1")
-        else:
-            monkeypatch.delenv("SF_CUDA_CC_GENERIC", raising=False)
+        monkeypatch.setenv("STENCILFORGE_CC", TOOL + ("-generic" if generic else ""))
+        monkeypatch.setenv("SF_CUDA_CC_LOG", str(log))
+        return log
     return use
 
 
@@ -184,8 +186,9 @@ def _run_acoustic(ref, shape, order, fwd, seed):
 @pytest.mark.parametrize("shape,order,fwd", ACOUSTIC)
 def test_reference_pipeline_on_gpu_acoustic(sf, ref, cuda_cc_env, shape, order, fwd, generic):
     want = _run_acoustic(ref, shape, order, fwd, 7)          # reference, gcc
-    cuda_cc_env(generic)
+    log = cuda_cc_env(generic)
     got = _run_acoustic(ref, shape, order, fwd, 7)           # reference, sf-cuda-cc
+    assert log.read_text().split()[0] == ("generic" if generic else "acoustic")
     for name in want:
         assert np.array_equal(got[name].view(np.uint32), want[name].view(np.uint32)), name
 
@@ -202,6 +205,7 @@ def test_reference_pipeline_on_gpu_diffusion(sf, ref, cuda_cc_env, order, generi
         op.apply()
         return op.get("u", np.float32, (2, 70, 66))
     want = run()
-    cuda_cc_env(generic)
+    log = cuda_cc_env(generic)
     got = run()
+    assert log.read_text().split()[0] == ("generic" if generic else "diffusion")
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
