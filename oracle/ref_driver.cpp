@@ -31,6 +31,7 @@ namespace {
 
 thread_local std::string g_err;
 thread_local std::string g_text;
+thread_local BlockingPlan g_blocking; // applied to the next build (opt.hpp:10-15)
 
 struct Handle {
     std::unique_ptr<Grid> grid_owner; // diffusion
@@ -73,6 +74,15 @@ extern "C" {
 const char* sfref_last_error() { return g_err.c_str(); }
 
 void sfref_set_threads(int n) { omp_set_num_threads(n); }
+
+// Blocking plan for the next acoustic/diffusion build: sizes for the spatial
+// dimensions "x", "y", "z" (grid.cpp:47); size 0 leaves a dimension unblocked.
+void sfref_set_blocking(int n, const long* sizes) {
+    static const char* names[3] = {"x", "y", "z"};
+    g_blocking = BlockingPlan{};
+    for (int d = 0; d < n && d < 3; ++d)
+        if (sizes[d] > 0) g_blocking.block[names[d]] = sizes[d];
+}
 int sfref_max_threads() { return omp_get_max_threads(); }
 
 // Acoustic forward (forward != 0) or adjoint operator, built but not run.
@@ -97,6 +107,7 @@ void* sfref_acoustic_build(int ndim, const long* shape, int boundary_width,
         m.v_bottom = v_bottom;
         if (nsrc > 0) m.src_coords = unpack(nsrc, ndim, src_coords);
         if (nrec > 0) m.rec_coords = unpack(nrec, ndim, rec_coords);
+        m.blocking = g_blocking;
         h->acoustic = acoustic_build(m, forward != 0);
         h->op = h->acoustic.op.get();
         h->grid = h->acoustic.grid.get();
@@ -136,6 +147,7 @@ void* sfref_diffusion_build(long nx, long ny, long alpha_num, long alpha_den,
         c.dx = c.dy = Rational(dx_num, dx_den);
         c.nt = nt;
         c.order = order;
+        c.blocking = g_blocking;
         h->dt = c.dt().to_double();
         h->diffusion = make_diffusion_operator(c);
         h->op = h->diffusion.op.get();

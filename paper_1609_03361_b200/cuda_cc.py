@@ -80,6 +80,7 @@ class Program:
 
 
 LOOP_RE = re.compile(r"^for \(int (\w+) = (.+?); \1 (<|>=) (.+?); \1 ([+-])= (\d+)\)$")
+CAP_RE = re.compile(r"^const int (\w+)_hi = \((\w+) \+ (\d+) < (\w+)\) \? \2 \+ \3 : \4;$")
 ALIAS_RE = re.compile(r"^(t\d+) = \((\w+)(?: \+ (\d+))?\) % (\d+);$")
 
 
@@ -162,8 +163,13 @@ def parse(src: str) -> Program:
                     nodes.extend(body)
                 pragma = ""
                 continue
-            if ln.startswith("const int ") and "_hi" in ln:
-                raise Unsupported("blocked loops")
+            cm = CAP_RE.match(ln)
+            if cm:
+                # remainder bound of a blocked loop (codegen.cpp:291-300)
+                nodes.append(Node("cap", var=cm.group(1), lo=cm.group(2), hi=cm.group(4),
+                                  step=int(cm.group(3))))
+                pos += 1
+                continue
             if ln.endswith(";"):
                 kind = "decl" if ln.startswith("const ") else "assign"
                 nodes.append(Node(kind, text=ln[:-1]))
@@ -175,7 +181,53 @@ def parse(src: str) -> Program:
         roots, pos = parse_block_top(lines, pos, parse_block)
     else:
         raise Unsupported("no loop nest")
-    return Program(entry, params, arrays, alias_names, roots)
+    return Program(entry, params, arrays, alias_names, unblock(roots))
+
+
+def _caps(nodes):
+    for n in nodes:
+        if n.kind == "cap":
+            yield n
+        yield from _caps(n.body)
+
+
+def _rebound(nodes, var, bvar, lo, hi, size):
+    """Give loop `var` (lo = bvar, hi = var_hi) the block loop's full range and
+    drop its cap."""
+    out = []
+    for n in nodes:
+        if n.kind == "cap" and n.var == var:
+            if n.lo != bvar or n.hi != hi or n.step != size:
+                raise Unsupported("cap")
+            continue
+        if n.kind == "loop":
+            n.body = _rebound(n.body, var, bvar, lo, hi, size)
+            if n.var == var:
+                if n.lo != bvar or n.hi != f"{var}_hi" or n.step != 1:
+                    raise Unsupported("blocked loop bounds")
+                n.lo, n.hi = lo, hi
+        out.append(n)
+    return out
+
+
+def unblock(nodes):
+    """Undo loop blocking (opt.cpp:136-200): a block loop `for (vb = lo; vb < hi;
+    vb += S)` over `for (v = vb; v < min(vb + S, hi); ...)` visits exactly the
+    points of `for (v = lo; v < hi; ...)`, and the reference only blocks
+    parallelisable dimensions (opt.cpp:167-169), whose points are independent;
+    the GPU schedule is chosen here instead."""
+    out = []
+    for n in nodes:
+        if n.kind == "loop":
+            n.body = unblock(n.body)
+            caps = [c for c in _caps(n.body) if c.lo == n.var]
+            if caps:
+                if len(caps) != 1 or n.descending or n.step != caps[0].step:
+                    raise Unsupported("block loop")
+                out.extend(_rebound(n.body, caps[0].var, n.var, n.lo, n.hi, n.step))
+                continue
+        out.append(n)
+    return out
 
 
 def parse_block_top(lines, pos, parse_block):

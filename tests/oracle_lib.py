@@ -210,6 +210,12 @@ class Ref:
         lib.sfref_interp_weights.argtypes = [C.c_int, _f64p, C.c_double, _i64p,
                                              C.POINTER(C.c_long), _f64p]
         lib.sfref_set_threads.argtypes = [C.c_int]
+        lib.sfref_set_blocking.argtypes = [C.c_int, C.POINTER(C.c_long)]
+
+    def set_blocking(self, sizes=()):
+        """Blocking plan (x, y, z sizes; 0 = unblocked) for the next builds."""
+        arr = (C.c_long * 3)(*(list(sizes) + [0] * (3 - len(sizes))))
+        self.lib.sfref_set_blocking(3, arr)
 
     def error(self):
         return self.lib.sfref_last_error().decode()

@@ -86,6 +86,29 @@ def test_lifted_diffusion_constants_match_library(ref, order):
     assert np.array_equal(np.asarray(got.cj, np.float32), cj)
 
 
+BLOCKINGS = [(8, 0, 16), (4, 4, 4), (0, 3, 0)]
+
+
+@needs_ref
+@pytest.mark.parametrize("blocking", BLOCKINGS)
+def test_blocked_sources_are_unblocked(ref, blocking):
+    """AcousticModel/DiffusionConfig::blocking (opt.cpp:136-200) wraps the
+    nest in block loops with capped inner bounds; the front end restores the
+    plain nest and still recognises the operator with the same constants."""
+    from paper_1609_03361_b200 import cuda_cc
+    plain = cuda_cc.recognise(cuda_cc.parse(ref_acoustic(ref, _case((26, 24, 22), 4), True)
+                                            .source()))
+    ref.set_blocking(blocking)
+    try:
+        src = ref_acoustic(ref, _case((26, 24, 22), 4), True).source()
+        dsrc = ref_diffusion(ref, 50, 40, (1, 2), (1, 10), 5, 4).source()
+    finally:
+        ref.set_blocking()
+    assert "_hi = " in src
+    assert cuda_cc.recognise(cuda_cc.parse(src)) == plain
+    assert isinstance(cuda_cc.recognise(cuda_cc.parse(dsrc)), cuda_cc.DiffusionOp)
+
+
 def test_unrecognised_source_falls_back_to_generic():
     from paper_1609_03361_b200 import cuda_cc
     src = """#include <math.h>
@@ -166,8 +189,12 @@ def cuda_cc_env(monkeypatch, tmp_path):
     return use
 
 
-def _run_acoustic(ref, shape, order, fwd, seed):
-    op = ref_acoustic(ref, _case(shape, order), fwd)
+def _run_acoustic(ref, shape, order, fwd, seed, blocking=()):
+    ref.set_blocking(blocking)
+    try:
+        op = ref_acoustic(ref, _case(shape, order), fwd)
+    finally:
+        ref.set_blocking()
     rng = np.random.default_rng(seed)
     field = "u" if fwd else "v"
     if not fwd:
@@ -188,6 +215,19 @@ def test_reference_pipeline_on_gpu_acoustic(sf, ref, cuda_cc_env, shape, order, 
     want = _run_acoustic(ref, shape, order, fwd, 7)          # reference, gcc
     log = cuda_cc_env(generic)
     got = _run_acoustic(ref, shape, order, fwd, 7)           # reference, sf-cuda-cc
+    assert log.read_text().split()[0] == ("generic" if generic else "acoustic")
+    for name in want:
+        assert np.array_equal(got[name].view(np.uint32), want[name].view(np.uint32)), name
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("blocking", BLOCKINGS)
+def test_reference_pipeline_on_gpu_blocked(sf, ref, cuda_cc_env, blocking, generic):
+    want = _run_acoustic(ref, (26, 24, 22), 4, False, 3, blocking)
+    log = cuda_cc_env(generic)
+    got = _run_acoustic(ref, (26, 24, 22), 4, False, 3, blocking)
     assert log.read_text().split()[0] == ("generic" if generic else "acoustic")
     for name in want:
         assert np.array_equal(got[name].view(np.uint32), want[name].view(np.uint32)), name
