@@ -580,8 +580,118 @@ extern "C" int {entry}(float* u) {{
 """
 
 
+def array_refs(text: str):
+    """[(name, [subscript, ...])] for every `name[..][..]` in an expression."""
+    out = []
+    for m in re.finditer(r"\b([A-Za-z_]\w*)\[", text):
+        if m.start() > 0 and text[m.start() - 1] in "]":
+            continue
+        name, i, subs = m.group(1), m.end() - 1, []
+        while i < len(text) and text[i] == "[":
+            depth, j = 0, i
+            while True:
+                depth += {"[": 1, "]": -1}.get(text[j], 0)
+                if depth == 0:
+                    break
+                j += 1
+            subs.append(text[i + 1:j].strip())
+            i = j + 1
+        out.append((name, subs))
+    return out
+
+
+def _statements(nodes):
+    for n in nodes:
+        if n.kind in ("assign", "decl"):
+            yield n
+        yield from _statements(n.body)
+
+
+def _loop_vars(node):
+    while node.kind == "loop":
+        yield node.var
+        node = node.body[0] if len(node.body) == 1 else Node("leaf")
+
+
+def parallel_safe(nest: Node, aliases) -> bool:
+    """Whether every point of a perfect loop nest can run concurrently.
+
+    Conservative dependence test on the statement text: each written array
+    element must be addressed injectively by the nest's variables (`v`, `v±c`,
+    host-fixed scalars, literals — no indirection, so the sequential injection
+    loops, whose corners may collide, stay sequential), and every read of a
+    written array must be the same element or a different time slot (distinct
+    modulo aliases of one alias block, codegen.cpp:336-354)."""
+    try:
+        levels, inner = nest_of(nest)
+    except (Unsupported, ValueError):
+        return False
+    vars_ = {v for v, _, _ in levels}
+    if any(n.kind not in ("assign", "decl") for n in inner):
+        return False
+    writes = {}
+    for st in inner:
+        if st.kind != "assign":
+            continue
+        lhs = st.text.split(" = ", 1)[0]
+        refs = array_refs(lhs)
+        if len(refs) != 1 or refs[0][0] + "".join(f"[{x}]" for x in refs[0][1]) != lhs:
+            return False
+        name, subs = refs[0]
+        used = []
+        for sub in subs:
+            m = re.match(r"^(\w+)(?: [+-] \d+)?$", sub)
+            if not m:
+                return False
+            if m.group(1) in vars_:
+                used.append(m.group(1))
+        if sorted(used) != sorted(vars_):
+            return False
+        if writes.setdefault(name, subs) != subs:
+            return False
+    def distinct(a, b):
+        # provably different elements: some subscript pair differs by a
+        # non-zero constant on the same loop-invariant base, or names two
+        # different time slots of one alias block
+        for x, y in zip(a, b):
+            if x in aliases and y in aliases:
+                if x != y:
+                    return True
+                continue
+            mx = re.match(r"^(\w+)(?: ([+-]) (\d+))?$", x)
+            my = re.match(r"^(\w+)(?: ([+-]) (\d+))?$", y)
+            if not (mx and my):
+                continue
+            if mx.group(1) in vars_ or my.group(1) in vars_:
+                continue
+            ox = int(mx.group(3) or 0) * (-1 if mx.group(2) == "-" else 1)
+            oy = int(my.group(3) or 0) * (-1 if my.group(2) == "-" else 1)
+            if mx.group(1).isdigit() and my.group(1).isdigit():
+                if int(mx.group(1)) + ox != int(my.group(1)) + oy:
+                    return True
+            elif mx.group(1) == my.group(1) and ox != oy:
+                return True
+        return False
+
+    for st in inner:
+        rhs = st.text.split(" = ", 1)[1]
+        for name, subs in array_refs(rhs):
+            if name not in writes or subs == writes[name]:
+                continue
+            if distinct(subs, writes[name]):
+                continue
+            return False
+    return True
+
+
 def emit_generic(prog: Program) -> str:
-    """Statement-for-statement CUDA translation of the generated nest."""
+    """Statement-for-statement CUDA translation of the generated nest.
+
+    Host-level structure (time loop, alias block, any loop that is not a
+    parallel nest but holds loops) runs on the host, in order, on one stream;
+    each parallel-safe perfect nest becomes one thread-per-point kernel; any
+    other loop (the `omp single` injection/sampling loops, recurrences) runs in
+    a one-thread kernel so its sequential order is kept."""
     arr_decl = []
     for ctype, name in prog.params:
         a = prog.arrays[name]
@@ -593,22 +703,8 @@ def emit_generic(prog: Program) -> str:
     decls = "\n".join(arr_decl)
     params_dev = ", ".join(f"{c} *{n}_vec" for c, n in prog.params)
     args_dev = ", ".join(f"d_{n}" for _, n in prog.params)
-    kernels = []
-    launches = []
-    counter = [0]
-    scalars = prog.alias_names
-
-    def scalar_params(tv):
-        ps = [f"int {s}" for s in scalars]
-        if tv:
-            ps.append(f"int {tv}")
-        return ", ".join(ps)
-
-    def scalar_args(tv):
-        a = list(scalars)
-        if tv:
-            a.append(tv)
-        return ", ".join(a)
+    aliases = set(prog.alias_names)
+    kernels, host = [], []
 
     def stmts(nodes, indent):
         out = []
@@ -626,23 +722,19 @@ def emit_generic(prog: Program) -> str:
                 raise Unsupported(f"node {n.kind} inside a kernel")
         return out
 
-    def kernel_for(node: Node, tv):
-        k = counter[0]
-        counter[0] += 1
-        extra = scalar_params(tv)
-        sig = f"{params_dev}" + (f", {extra}" if extra else "")
-        if "single" in node.pragma or node.var == "p":
-            body = "\n".join(stmts([node], 8))
+    def launch(node_list, scalars, parallel):
+        k = len(kernels)
+        scalars = list(prog.alias_names) + list(scalars)
+        sc = [f"int {v}" for v in scalars]
+        sig = ", ".join([params_dev] + sc)
+        call_args = ", ".join([args_dev] + list(scalars))
+        if not parallel:
+            body = "\n".join(stmts(node_list, 8))
             kernels.append(f"__global__ void sfk{k}({sig}) {{\n{decls}\n    {{\n{body}\n    }}\n}}")
-            launches.append(f"sfk{k}<<<1, 1>>>({args_dev}" + (f", {scalar_args(tv)}" if extra else "")
-                            + ");")
-            return
-        levels, inner = nest_of(node)
-        if len(levels) > 3:
-            raise Unsupported("deep nest")
+            return f"sfk{k}<<<1, 1>>>({call_args});"
+        levels, inner = nest_of(node_list[0])
         axes = ["x", "y", "z"]
-        lines = []
-        conds = []
+        lines, conds = [], []
         for depth, (var, lo, hi) in enumerate(reversed(levels)):
             ax = axes[depth]
             lines.append(f"    const int {var} = {lo} + (int)(blockIdx.{ax} * blockDim.{ax} + threadIdx.{ax});")
@@ -651,39 +743,46 @@ def emit_generic(prog: Program) -> str:
         kernels.append(f"__global__ void sfk{k}({sig}) {{\n{decls}\n" + "\n".join(lines)
                        + f"\n    if ({' && '.join(conds)}) {{\n{body}\n    }}\n}}")
         ext = [hi - lo for _, lo, hi in reversed(levels)] + [1] * (3 - len(levels))
-        bx = [32, 8, 1][: len(levels)] + [1] * (3 - len(levels))
-        if len(levels) == 1:
-            bx = [256, 1, 1]
-        grid = ", ".join(f"({e} + {b} - 1) / {b}" for e, b in zip(ext, bx))
-        launches.append(f"sfk{k}<<<dim3({grid}), dim3({bx[0]}, {bx[1]}, {bx[2]})>>>({args_dev}"
-                        + (f", {scalar_args(tv)}" if extra else "") + ");")
+        block = {1: [256, 1, 1], 2: [32, 8, 1], 3: [32, 4, 2]}[len(levels)]
+        grid = ", ".join(f"{(e + b - 1) // b}" for e, b in zip(ext, block))
+        if any(e <= 0 for e in ext):
+            return ";  /* empty nest */"
+        return f"sfk{k}<<<dim3({grid}), dim3({block[0]}, {block[1]}, {block[2]})>>>({call_args});"
 
-    host = []
-
-    def walk(nodes, tv, indent):
+    def walk(nodes, scalars, indent):
+        pad = " " * indent
         for n in nodes:
             if n.kind == "aliases":
+                tv = scalars[-1] if scalars else None
                 for name, off, mod in n.aliases:
+                    if tv is None:
+                        raise Unsupported("alias block outside a loop")
                     rhs = f"({tv} + {off}) % {mod}" if off else f"({tv}) % {mod}"
-                    host.append(" " * indent + f"{name} = {rhs};")
-            elif n.kind == "loop" and tv is None and n.var.startswith("i") and not n.pragma and \
-                    any(c.kind == "aliases" for c in n.body):
-                cmp = ">=" if n.descending else "<"
-                op_ = "-=" if n.descending else "+="
-                host.append(" " * indent + f"for (int {n.var} = {n.lo}; {n.var} {cmp} {n.hi}; "
-                            f"{n.var} {op_} {n.step}) {{")
-                walk(n.body, n.var, indent + 4)
-                host.append(" " * indent + "}")
+                    host.append(pad + f"{name} = {rhs};")
             elif n.kind == "loop":
-                kernel_for(n, tv)
-                host.append(" " * indent + launches[-1])
+                try:
+                    levels, _ = nest_of(n)
+                    nested_ok = len(levels) <= 3
+                except (Unsupported, ValueError):
+                    nested_ok = False
+                if nested_ok and parallel_safe(n, aliases):
+                    host.append(pad + launch([n], scalars, True))
+                elif any(c.kind in ("loop", "aliases") for c in n.body):
+                    cmp = ">=" if n.descending else "<"
+                    op_ = "-=" if n.descending else "+="
+                    host.append(pad + f"for (int {n.var} = {n.lo}; {n.var} {cmp} {n.hi}; "
+                                f"{n.var} {op_} {n.step}) {{")
+                    walk(n.body, scalars + [n.var], indent + 4)
+                    host.append(pad + "}")
+                else:
+                    host.append(pad + launch([n], scalars, False))
+            elif n.kind in ("assign", "decl"):
+                host.append(pad + launch([n], scalars, False))
             else:
                 raise Unsupported(f"host-level {n.kind}")
 
-    # time loop = the outermost loop that holds the alias block (or none)
-    walk(prog.roots, None, 8)
-    copies_in = []
-    copies_out = []
+    walk(prog.roots, [], 8)
+    copies_in, copies_out = [], []
     for ctype, name in prog.params:
         copies_in.append(f"        size_t n_{name} = extent_bytes({name}_vec, {row_bytes(prog, ctype, name)});\n"
                          f"        {ctype}* d_{name} = 0;\n"
@@ -693,6 +792,7 @@ def emit_generic(prog: Program) -> str:
                           f"        cudaFree(d_{name});")
     alias_decl = "".join(f"        int {a} = 0;\n" for a in prog.alias_names)
     host_params = ", ".join(f"{c} *{n}_vec" for c, n in prog.params)
+    nl = "\n"
     return f"""// generated by sf-cuda-cc: statement-for-statement CUDA translation
 #include <cuda_runtime.h>
 #include <malloc.h>
@@ -706,14 +806,21 @@ static size_t extent_bytes(const void* p, size_t row) {{
     return row ? n / row * row : n;
 }}
 
-{chr(10).join(kernels)}
+// powf with a non-integral exponent (codegen.cpp:170-176): evaluated in double
+// and rounded once, as glibc's powf does
+__device__ __forceinline__ float sf_powf(float a, float b) {{
+    return (float)pow((double)a, (double)b);
+}}
+#define powf sf_powf
+
+{nl.join(kernels)}
 
 extern "C" int {prog.entry}({host_params}) {{
     {{
-{chr(10).join(copies_in)}
-{alias_decl}{chr(10).join(host)}
+{nl.join(copies_in)}
+{alias_decl}{nl.join(host)}
         if (cudaDeviceSynchronize() != cudaSuccess) return 3;
-{chr(10).join(copies_out)}
+{nl.join(copies_out)}
     }}
     return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }}
