@@ -200,6 +200,13 @@ int sf_plan_attach_nccl(sf_plan *plan, const void *id, int nranks, int rank);
 int sf_plan_save_buffer(sf_plan *plan, const char *name, const char *path);
 int sf_plan_load_buffer(sf_plan *plan, const char *name, const char *path);
 
+/* Text dumps from the device mirror: dump_csv (grid.cpp:256-273; 2D grid
+ * functions only, `slot` selects the time slot of u/v) and save_series_text
+ * (sparse.cpp:215-227; "src"/"rec", one row per time step, space-separated).
+ * Numbers are formatted like `std::ostream << double` (printf "%g"). */
+int sf_plan_dump_csv(sf_plan *plan, const char *name, const char *path, long slot);
+int sf_plan_save_series_text(sf_plan *plan, const char *name, const char *path);
+
 /* ---- GPU autotune (Operator::autotune, op.cpp:169-221) -----------------
  * Times every stencil kernel variant compiled for the plan's order (kernel
  * family, tile, pipeline depth) on `tune_steps` steps of the resident state,

@@ -273,4 +273,23 @@ int sfref_load_buffer(void* hp, const char* name, const char* path) {
     Handle* h = static_cast<Handle*>(hp);
     return guard([&] { load_buffer(*h->grid->find(name), path); });
 }
+// dump_csv (grid.cpp:256-273) and save_series_text (sparse.cpp:215-227)
+int sfref_dump_csv(void* hp, const char* name, const char* path, long slot) {
+    Handle* h = static_cast<Handle*>(hp);
+    return guard([&] { dump_csv(*h->grid->find(name), path, slot); });
+}
+int sfref_save_series_text(void* hp, const char* name, const char* path) {
+    Handle* h = static_cast<Handle*>(hp);
+    return guard([&] { save_series_text(*h->grid->find(name), path); });
+}
+// load_series_column (sparse.cpp:205-213): returns the count, fills up to cap
+long sfref_load_series_column(const char* path, double* out, long cap) {
+    long n = -1;
+    guard([&] {
+        std::vector<double> v = load_series_column(path);
+        n = static_cast<long>(v.size());
+        for (long i = 0; i < n && i < cap; ++i) out[i] = v[i];
+    });
+    return n;
+}
 }

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import re
 from dataclasses import dataclass, field
 from fractions import Fraction
 
@@ -288,6 +289,14 @@ class Operator:
         """load_buffer (grid.cpp:236-254) straight into the HBM mirror."""
         check(lib.sf_plan_load_buffer(self._plan, name.encode(), str(path).encode()))
 
+    def dump_csv(self, name, path, slot=0):
+        """dump_csv (grid.cpp:256-273) of a 2D grid function from HBM."""
+        check(lib.sf_plan_dump_csv(self._plan, name.encode(), str(path).encode(), slot))
+
+    def save_series_text(self, name, path):
+        """save_series_text (sparse.cpp:215-227) of "src"/"rec" from HBM."""
+        check(lib.sf_plan_save_series_text(self._plan, name.encode(), str(path).encode()))
+
     KINDS = {0: "per-thread-load", 1: "tma", 2: "vector-tma", 3: "queue-vector-tma"}
 
     def autotune(self, tune_nt=5, repeats=3):
@@ -317,6 +326,29 @@ class Operator:
 
 # ---------------------------------------------------------------------------
 # acoustic application (acoustic.hpp:17-91)
+
+_NUM = re.compile(r"[+-]?(?:\d+\.?\d*|\.\d+)(?:[eE][+-]?\d+)?")
+
+
+def load_series_column(path) -> np.ndarray:
+    """load_series_column (sparse.cpp:205-213): whitespace-separated numbers
+    read with `in >> double` until the first token that does not parse (a
+    numeric prefix is still taken, as the stream extraction does)."""
+    try:
+        with open(path) as f:
+            text = f.read()
+    except OSError as e:
+        raise SfError(f"cannot open series file: {path}") from e
+    out = []
+    for tok in text.split():
+        m = _NUM.match(tok)
+        if not m:
+            break
+        out.append(float(m.group(0)))
+        if m.end() != len(tok):
+            break
+    return np.asarray(out, np.float64)
+
 
 def ricker_wavelet(f0, t, t0):
     return lib.sf_ricker(f0, t, t0)

@@ -1949,6 +1949,71 @@ extern "C" int sf_plan_load_buffer(sf_plan* p, const char* name, const char* pat
     });
 }
 
+// Text dumps (dump_csv, grid.cpp:256-273; save_series_text, sparse.cpp:215-227):
+// values are written as `std::ostream << double` does by default, i.e. printf
+// "%g" (six significant digits) of the f32 value widened to double.
+namespace sfb {
+void put_g(FILE* f, float x) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%g", static_cast<double>(x));
+    std::fputs(buf, f);
+}
+}  // namespace sfb
+
+extern "C" int sf_plan_dump_csv(sf_plan* p, const char* name, const char* path, long slot) {
+    using namespace sfb;
+    if (!p || !name || !path) return SF_ERR_INVALID;
+    return guard([&] {
+        if (p->kind == sf_plan::FWI) throw Status(SF_ERR_INVALID, "FWI plans have no buffers");
+        const int i = find_arg(*p, name);
+        const BufferView v = buffer_view(*p, i);
+        const bool field = p->kind == sf_plan::DIFFUSION || i <= 2;
+        const bool timed = p->kind == sf_plan::DIFFUSION || i == 0;
+        if (!field || p->ndim != 2) throw Status(SF_ERR_INVALID, "csv dump supports 2D grids only");
+        const long slots = timed ? static_cast<long>(v.extents[0]) : 1;
+        if (timed && (slot < 0 || slot >= slots))
+            throw Status(SF_ERR_INVALID, "slot out of range");
+        std::vector<float> host(static_cast<size_t>(p->arg_bytes.at(i)) / 4);
+        transfer_arg(*p, i, host.data(), true);
+        const long n0 = p->n[0], n1 = p->n[1];
+        const float* base = host.data() + (timed ? slot * n0 * n1 : 0);
+        FILE* f = std::fopen(path, "w");
+        if (!f) throw Status(SF_ERR_INVALID, std::string("cannot open for write: ") + path);
+        for (long a = 0; a < n0; ++a) {
+            for (long b = 0; b < n1; ++b) {
+                if (b) std::fputc(',', f);
+                put_g(f, base[a * n1 + b]);
+            }
+            std::fputc('\n', f);
+        }
+        if (std::fclose(f) != 0) throw Status(SF_ERR_INVALID, std::string("short write: ") + path);
+    });
+}
+
+extern "C" int sf_plan_save_series_text(sf_plan* p, const char* name, const char* path) {
+    using namespace sfb;
+    if (!p || !name || !path) return SF_ERR_INVALID;
+    return guard([&] {
+        if (p->kind != sf_plan::ACOUSTIC) throw Status(SF_ERR_INVALID, "no sparse series in this plan");
+        const int i = find_arg(*p, name);
+        if (i != 3 && i != 6) throw Status(SF_ERR_INVALID, std::string(name) + " is not a series");
+        const BufferView v = buffer_view(*p, i);
+        const long nt = v.extents[0], np = v.extents[1];
+        std::vector<float> host(static_cast<size_t>(nt * np));
+        if (!host.empty()) transfer_arg(*p, i, host.data(), true);
+        FILE* f = std::fopen(path, "w");
+        if (!f) throw Status(SF_ERR_INVALID, std::string("cannot open for write: ") + path);
+        for (long t = 0; t < nt; ++t) {
+            for (long q = 0; q < np; ++q) {
+                if (q) std::fputc(' ', f);
+                put_g(f, host[t * np + q]);
+            }
+            std::fputc('\n', f);
+        }
+        if (std::fclose(f) != 0) throw Status(SF_ERR_INVALID, std::string("short write: ") + path);
+    });
+}
+
 extern "C" {
 
 const char* sf_last_error(void) { return sfb::g_error.c_str(); }

@@ -385,3 +385,58 @@ def test_hbm_buffer_io_interchanges_with_reference(sf, ref, tmp_path):
     assert np.array_equal(bits(s.field.data), bits(op.get("u", np.float32, (3, 24, 24, 20))))
     with pytest.raises(sf.SfError):
         s.op.load_buffer("m", path)  # shape/rank mismatch is rejected
+
+
+def test_text_dumps_match_reference(sf, ref, tmp_path):
+    """dump_csv (grid.cpp:256-273) and save_series_text (sparse.cpp:215-227)
+    from HBM are byte-identical to the reference's own files; the series
+    reader load_series_column (sparse.cpp:205-213) reads them back alike."""
+    import ctypes as C
+    from oracle_lib import AcousticCase, ref_acoustic, ref_diffusion
+    ref.lib.sfref_dump_csv.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_long]
+    ref.lib.sfref_save_series_text.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p]
+    ref.lib.sfref_load_series_column.restype = C.c_long
+    ref.lib.sfref_load_series_column.argtypes = [C.c_char_p, C.c_void_p, C.c_long]
+    model = sf.AcousticModel(shape=(48, 44), nt=60, boundary_width=6, spacing=10.0,
+                             space_order=4)
+    s = sf.acoustic_forward(model)
+    op = ref_acoustic(ref, AcousticCase(shape=(48, 44), nt=60, boundary_width=6,
+                                        spacing=10.0, space_order=4), True)
+    op.apply()
+    files = []
+    for name, slot in [("u", 0), ("u", 1), ("u", 2), ("m", 0), ("eta", 0)]:
+        mine, theirs = tmp_path / f"{name}{slot}.csv", tmp_path / f"{name}{slot}_ref.csv"
+        s.op.dump_csv(name, mine, slot)
+        assert ref.lib.sfref_dump_csv(op.h, name.encode(), str(theirs).encode(), slot) == 0
+        files.append((mine, theirs))
+    for name in ("rec", "src"):
+        mine, theirs = tmp_path / f"{name}.txt", tmp_path / f"{name}_ref.txt"
+        s.op.save_series_text(name, mine)
+        assert ref.lib.sfref_save_series_text(op.h, name.encode(), str(theirs).encode()) == 0
+        files.append((mine, theirs))
+    for mine, theirs in files:
+        assert mine.read_bytes() == theirs.read_bytes(), mine.name
+    # the reader: same numbers as the reference's parser
+    path = files[-2][0]
+    got = sf.load_series_column(path)
+    want = np.zeros(got.size + 8)
+    n = ref.lib.sfref_load_series_column(str(path).encode(), want.ctypes.data, want.size)
+    assert n == got.size and np.array_equal(got, want[:n])
+    # diffusion (time-varying, 2 slots) and the rejections
+    d = sf.make_diffusion_operator(sf.DiffusionConfig(nx=40, ny=36, nt=7))
+    d.u.data[...] = np.random.default_rng(3).random(d.u.data.shape, dtype=np.float32)
+    d.op.apply()
+    rop = ref_diffusion(ref, 40, 36, (1, 2), (1, 39), 7, 2)
+    rop.set("u", d.u.data)
+    for slot in (0, 1):
+        mine, theirs = tmp_path / f"d{slot}.csv", tmp_path / f"d{slot}_ref.csv"
+        d.op.dump_csv("u", mine, slot)
+        assert ref.lib.sfref_dump_csv(rop.h, b"u", str(theirs).encode(), slot) == 0
+        assert mine.read_bytes() == theirs.read_bytes()
+    with pytest.raises(sf.SfError):
+        d.op.dump_csv("u", tmp_path / "bad.csv", 2)
+    s3 = sf.acoustic_forward(sf.AcousticModel(shape=(24, 24, 20), nt=5, boundary_width=4))
+    with pytest.raises(sf.SfError):
+        s3.op.dump_csv("u", tmp_path / "bad3d.csv", 0)   # 2D grids only
+    with pytest.raises(sf.SfError):
+        s3.op.save_series_text("m", tmp_path / "bad.txt")
