@@ -422,10 +422,16 @@ size_t tma_smem_bytes(int r, int nx, int stages) {
 }
 
 // ---- vectorised TMA path (4 consecutive a2 points per thread) -------------
+// tile_nx selects the tile width for the vector kernel: 2 -> 64-wide tiles
+// (16 lanes per row), 1 -> 32-wide (8 lanes per row, 4-warp CTAs only)
 template <bool FWD>
-const void* vec_ptr(int r, int warps) {
+const void* vec_ptr(int r, int warps, int nx = 2) {
 #define SF_V(RR)                                                                              \
     case RR:                                                                                  \
+        if (nx == 1)                                                                          \
+            return warps == 4 ? reinterpret_cast<const void*>(                                \
+                                    &acoustic3d_vec_kernel<RR, FWD, 4, false, 8>)             \
+                              : nullptr;                                                      \
         return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4>) \
                           : reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 8>);
     switch (r) {
@@ -435,11 +441,12 @@ const void* vec_ptr(int r, int warps) {
 #undef SF_V
 }
 
-size_t vec_smem_bytes(int r, int warps, int stages, int npme = 3) {
+size_t vec_smem_bytes(int r, int warps, int stages, int npme = 3, int nx = 2) {
     const int ra = (r + 3) / 4 * 4;
-    const int wb = 64 + 2 * ra, h = 2 * warps + 2 * r;
+    const int tx = 32 * nx, ty = 4 * warps / nx;
+    const int wb = tx + 2 * ra, h = ty + 2 * r;
     const int cur = (wb * h * 4 + 127) / 128 * 128;
-    const int pme = (64 * 2 * warps * 4 + 127) / 128 * 128;
+    const int pme = (tx * ty * 4 + 127) / 128 * 128;
     return 256 + static_cast<size_t>(2 * r + stages) * cur +
            static_cast<size_t>(stages) * npme * pme;
 }
@@ -504,11 +511,14 @@ void launch_vec_grad(int r, dim3 g, size_t smem, cudaStream_t st, const TmaStenc
 }
 
 template <bool FWD>
-void launch_vec(int r, int warps, dim3 g, size_t smem, cudaStream_t st, const TmaStencilArgs& A) {
+void launch_vec(int r, int warps, int nx, dim3 g, size_t smem, cudaStream_t st,
+                const TmaStencilArgs& A) {
     const dim3 b(32 * (warps + 1));  // + the TMA producer warp
 #define SF_V(RR)                                                                   \
     case RR:                                                                       \
-        if (warps == 4)                                                            \
+        if (nx == 1)                                                               \
+            acoustic3d_vec_kernel<RR, FWD, 4, false, 8><<<g, b, smem, st>>>(A);    \
+        else if (warps == 4)                                                       \
             acoustic3d_vec_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);              \
         else                                                                       \
             acoustic3d_vec_kernel<RR, FWD, 8><<<g, b, smem, st>>>(A);              \
@@ -559,10 +569,12 @@ void make_tensor_map(CUtensorMap* map, const Plan& p, const float* base, uint32_
 void setup_tma(Plan& p) {
     const int r = p.ac.radius;
     const int nx = p.tile_nx;
-    const uint32_t wb = static_cast<uint32_t>(p.use_vec ? 64 + 2 * ((r + 3) / 4 * 4)
+    // vector kernels: ring/queue (64 x 2*warps tiles) or ring with 32-wide tiles
+    const int vnx = p.use_vecq ? 2 : nx;
+    const uint32_t wb = static_cast<uint32_t>(p.use_vec ? 32 * vnx + 2 * ((r + 3) / 4 * 4)
                                                         : tma_box_width(r, nx));
-    const uint32_t ty = static_cast<uint32_t>(p.use_vec ? 2 * p.vec_warps : 8);
-    const uint32_t tx = static_cast<uint32_t>(p.use_vec ? 64 : 32 * nx);
+    const uint32_t ty = static_cast<uint32_t>(p.use_vec ? 4 * p.vec_warps / vnx : 8);
+    const uint32_t tx = static_cast<uint32_t>(p.use_vec ? 32 * vnx : 32 * nx);
     const uint32_t cy = ty + static_cast<uint32_t>(2 * r);
     for (int s = 0; s < 3; ++s) {
         if (p.slot[s]) {
@@ -599,16 +611,16 @@ void setup_tma(Plan& p) {
     }
     if (p.use_vec) {
         int stages = 3;
-        while (stages > 2 && vec_smem_bytes(r, p.vec_warps, stages) * 2 > 226 * 1024) --stages;
+        while (stages > 2 && vec_smem_bytes(r, p.vec_warps, stages, 3, nx) * 2 > 226 * 1024) --stages;
         if (const char* env = std::getenv("SF_TMA_STAGES")) {
             const int v = std::atoi(env);
             if (v >= 2 && v <= 16) stages = v;
         }
         if (p.stages_override >= 2) stages = p.stages_override;
         p.tma_stages = stages;
-        p.tma_smem = vec_smem_bytes(r, p.vec_warps, stages);
+        p.tma_smem = vec_smem_bytes(r, p.vec_warps, stages, 3, nx);
         for (int fwd = 0; fwd < 2; ++fwd) {
-            const void* fn = fwd ? vec_ptr<true>(r, p.vec_warps) : vec_ptr<false>(r, p.vec_warps);
+            const void* fn = fwd ? vec_ptr<true>(r, p.vec_warps, nx) : vec_ptr<false>(r, p.vec_warps, nx);
             if (!fn) throw Status(SF_ERR_INVALID, "vector stencil not compiled");
             SF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(p.tma_smem)));
@@ -803,9 +815,9 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
         }
         if (p.use_vec) {
             if (p.ac.forward)
-                launch_vec<true>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T);
+                launch_vec<true>(p.ac.radius, p.vec_warps, p.tile_nx, grid3, p.tma_smem, p.stream, T);
             else
-                launch_vec<false>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T);
+                launch_vec<false>(p.ac.radius, p.vec_warps, p.tile_nx, grid3, p.tma_smem, p.stream, T);
             return;
         }
         if (p.ac.forward)
@@ -1355,15 +1367,17 @@ void chunk_grid(const Plan& p, int64_t wx, int64_t wy, int per_sm, dim3* grid, i
 
 void set_grid(Plan& p) {
     const int r = p.ac.radius;
-    const int64_t wx = p.use_vec ? 64 : 32 * p.tile_nx;
-    const int64_t wy = p.use_vec ? 2 * p.vec_warps : p.tile_ty;
+    const int64_t wx = p.use_vecq ? 64 : 32 * p.tile_nx;
+    const int64_t wy = p.use_vecq ? 2 * p.vec_warps : p.use_vec ? 4 * p.vec_warps / p.tile_nx
+                                                                 : p.tile_ty;
     int per_sm = 0;
     if (p.use_vecq) {
         const void* fn = p.ac.forward ? vecq_ptr<true>(r, p.vec_warps) : vecq_ptr<false>(r, p.vec_warps);
         if (fn)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.vec_warps, p.tma_smem);
     } else if (p.use_vec) {
-        const void* fn = p.ac.forward ? vec_ptr<true>(r, p.vec_warps) : vec_ptr<false>(r, p.vec_warps);
+        const void* fn = p.ac.forward ? vec_ptr<true>(r, p.vec_warps, p.tile_nx)
+                                      : vec_ptr<false>(r, p.vec_warps, p.tile_nx);
         if (fn)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * (p.vec_warps + 1),
                                                           p.tma_smem);
@@ -1456,6 +1470,25 @@ void enable_tma(Plan& p) {
         p.vec_warps = (p.ac.radius <= 3 || p.kind == Plan::FWI) ? 4 : 8;
         if (const char* w = std::getenv("SF_VEC_WARPS"))
             if (p.kind != Plan::FWI) p.vec_warps = std::atoi(w) == 4 ? 4 : 8;
+        // tile width: 64 (16 lanes per row) unless 32-wide 4-warp tiles
+        // cover the interior with fewer padded points (FWI: 64 wide, one set
+        // of maps serves the forward and gradient kernels)
+        p.tile_nx = 2;
+        if (p.kind != Plan::FWI) {
+            const int r = p.ac.radius;
+            auto cover = [&](int nx, int warps) {
+                const int64_t tx = 32 * nx, ty = 4 * warps / nx;
+                return ((p.n[2] - r + tx - 1) / tx * tx) * ((p.n[1] - r + ty - 1) / ty * ty);
+            };
+            if (cover(1, 4) < cover(2, p.vec_warps)) {
+                p.tile_nx = 1;
+                p.vec_warps = 4;
+            }
+            if (const char* e = std::getenv("SF_VEC_NX")) {
+                p.tile_nx = std::atoi(e) == 1 ? 1 : 2;
+                if (p.tile_nx == 1) p.vec_warps = 4;
+            }
+        }
         setup_tma(p);
         p.use_tma = true;
         set_grid(p);
@@ -1739,9 +1772,11 @@ std::vector<StencilConfig> tune_candidates(const Plan& p) {
     if (r <= 3)
         for (int nx = 1; nx <= tma_max_nx(r); ++nx)
             for (int st : {2, 3}) out.push_back({1, nx, 8, 4, st});
-    if (r <= 4)
+    if (r <= 4) {
         for (int w : {4, 8})
             for (int st : {2, 3, 4}) out.push_back({2, 2, 2 * w, w, st});
+        for (int st : {2, 3, 4}) out.push_back({2, 1, 16, 4, st});
+    }
     if (r >= 5)
         for (int w : {4, 8})
             for (int st : {2, 3, 4}) out.push_back({3, 2, 2 * w, w, st});
