@@ -83,6 +83,13 @@ struct PointSet {
     int* cp = nullptr;
     float* cw = nullptr;
     std::vector<int32_t> host_ci;  // last uploaded indices (validated)
+    // host copy of the device CSR (change detection: a re-upload of the same
+    // points leaves the device buffers, and the graphs that use them, alone)
+    std::vector<int64_t> h_cells;
+    std::vector<int> h_start, h_cp;
+    std::vector<float> h_cw;
+    size_t cap_cells = 0, cap_contrib = 0;
+    uint64_t version = 0;  // bumped whenever the device CSR changes
 };
 
 } // namespace sfb
@@ -157,6 +164,18 @@ struct sf_plan {
     ZRange zr_lo, zr_hi, zr_in;
     cudaStream_t comm = nullptr;
     cudaEvent_t ev_band = nullptr, ev_comm = nullptr;
+    // fused sparse epilogue of the vector kernel: tile-sorted injection CSR
+    struct FusedSparse {
+        bool ok = false;          // built and every cell inside the tile grid
+        uint64_t key[8] = {};     // (csr version, grid, zchunk, tile, z-range)
+        int* tile_start = nullptr;
+        int64_t* cell = nullptr;
+        int* start = nullptr;
+        int* cp = nullptr;
+        float* cw = nullptr;
+        size_t cap_tiles = 0, cap_cells = 0, cap_contrib = 0;
+    } fused;
+    bool fused_disabled = false;  // SF_NO_FUSED_SPARSE=1
 
     ~sf_plan();
 };
@@ -232,6 +251,11 @@ void free_points(PointSet& s) {
 // Validate indices (the reference would index out of bounds silently) and
 // build the deterministic injection CSR: distinct target cells, each with its
 // (p, w[p][k]) contributions in ascending p.
+void clear_graphs(Plan& p) {
+    for (auto& kv : p.graphs) cudaGraphExecDestroy(kv.second);
+    p.graphs.clear();
+}
+
 void upload_points(Plan& p, PointSet& s, const float* series, const int* ci, const float* w,
                    bool injects) {
     const int corners = 1 << p.ndim;
@@ -302,23 +326,39 @@ void upload_points(Plan& p, PointSet& s, const float* series, const int* ci, con
         cp.push_back(0);
         cw.push_back(0.0f);
     }
-    dfree(s.cell_off);
-    dfree(s.start);
-    dfree(s.cp);
-    dfree(s.cw);
-    s.ncells = cs.empty() ? 0 : static_cast<int>(cells.size());
-    s.nband0 = cs.empty() ? 0 : nband0;
-    s.cell_off = dalloc<int64_t>(cells.size());
-    s.start = dalloc<int>(start.size());
-    s.cp = dalloc<int>(cp.size());
-    s.cw = dalloc<float>(cw.size());
-    // synchronous copies: the host vectors die at scope exit
+    const int ncells = cs.empty() ? 0 : static_cast<int>(cells.size());
+    const int nb0 = cs.empty() ? 0 : nband0;
+    if (s.cell_off && ncells == s.ncells && nb0 == s.nband0 && cells == s.h_cells &&
+        start == s.h_start && cp == s.h_cp && cw == s.h_cw)
+        return;  // same points: device CSR and captured graphs stay valid
+    // the CSR changed: captured graphs bake its sizes (and maybe pointers)
+    clear_graphs(p);
+    if (!s.cell_off || cells.size() > s.cap_cells || cp.size() > s.cap_contrib) {
+        dfree(s.cell_off);
+        dfree(s.start);
+        dfree(s.cp);
+        dfree(s.cw);
+        s.cap_cells = cells.size();
+        s.cap_contrib = cp.size();
+        s.cell_off = dalloc<int64_t>(s.cap_cells);
+        s.start = dalloc<int>(s.cap_cells + 1);
+        s.cp = dalloc<int>(s.cap_contrib);
+        s.cw = dalloc<float>(s.cap_contrib);
+    }
+    s.ncells = ncells;
+    s.nband0 = nb0;
+    // synchronous copies (earlier work on the stream may still read the CSR)
     SF_CUDA(cudaStreamSynchronize(p.stream));
     SF_CUDA(cudaMemcpy(s.cell_off, cells.data(), cells.size() * sizeof(int64_t),
                        cudaMemcpyHostToDevice));
     SF_CUDA(cudaMemcpy(s.start, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice));
     SF_CUDA(cudaMemcpy(s.cp, cp.data(), cp.size() * sizeof(int), cudaMemcpyHostToDevice));
     SF_CUDA(cudaMemcpy(s.cw, cw.data(), cw.size() * sizeof(float), cudaMemcpyHostToDevice));
+    s.h_cells = std::move(cells);
+    s.h_start = std::move(start);
+    s.h_cp = std::move(cp);
+    s.h_cw = std::move(cw);
+    ++s.version;
 }
 
 // ---------------------------------------------------------------------------
@@ -761,9 +801,17 @@ bool map_for(const Plan& p, const float* f, MapSel* m) {
     return false;
 }
 
+// Sparse work folded into the vector kernel's epilogue (TmaStencilArgs).
+struct Epilogue {
+    const PointSet* inj = nullptr;  // inject this step's row (tile-sorted CSR)
+    int64_t inj_row = 0;
+    const PointSet* smp = nullptr;  // sample the previous step from `cur`
+    int64_t smp_row = 0;
+};
+
 void launch_stencil(const Plan& p, float* out, const float* cur, const float* prev,
                     float* grad = nullptr, const float* uhist = nullptr,
-                    const sf_plan::ZRange* zr = nullptr) {
+                    const sf_plan::ZRange* zr = nullptr, const Epilogue* epi = nullptr) {
     if (zr && zr->z0 >= zr->z1) return;
     const dim3 grid3 = zr ? zr->grid : p.grid3;
     MapSel mc, mp, mo, mu;
@@ -814,6 +862,23 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
             return;
         }
         if (p.use_vec) {
+            if (epi && epi->inj && p.fused.ok && epi->inj->np > 0 && epi->inj->ncells > 0) {
+                T.inj_tile_start = p.fused.tile_start;
+                T.inj_cell = p.fused.cell;
+                T.inj_start = p.fused.start;
+                T.inj_cp = p.fused.cp;
+                T.inj_cw = p.fused.cw;
+                T.inj_row = epi->inj->series + epi->inj_row * epi->inj->np;
+                T.mfield = p.m;
+                T.inj_scale = p.ac.src_scale;
+            }
+            if (epi && epi->smp && epi->smp->np > 0) {
+                T.smp_field = cur;
+                T.smp_ci = epi->smp->ci;
+                T.smp_w = epi->smp->w;
+                T.smp_out = epi->smp->series + epi->smp_row * epi->smp->np;
+                T.smp_np = static_cast<int>(epi->smp->np);
+            }
             if (p.ac.forward)
                 launch_vec<true>(p.ac.radius, p.vec_warps, p.tile_nx, grid3, p.tma_smem, p.stream, T);
             else
@@ -999,10 +1064,13 @@ void launch_inject_sample(const Plan& p, const PointSet& inj, const PointSet& sm
     launch_sample(p, smp, field, row);
 }
 
+bool fused_sparse_active(const Plan& p);
+
 int64_t launches_per_step_of(const Plan& p) {
     if (p.kind == Plan::DIFFUSION) return 1;  // per step without temporal blocking
     if (p.nccl_comm && p.overlap) return 6;  // 3 stencil ranges, 2 injections, sampling
     if (p.nccl_comm && (p.has_lower || p.has_upper)) return 3;
+    if (fused_sparse_active(p)) return 1;  // + one sampling launch per step range
     const PointSet& inj = p.ac.forward ? p.src : p.rec;
     const PointSet& smp = p.ac.forward ? p.rec : p.src;
     return (inj.ncells <= kFusedSparseMax && smp.np <= kFusedSparseMax) ? 2 : 3;
@@ -1026,7 +1094,16 @@ StepSlots step_slots(const Plan& p, int64_t k, float* const* u) {
     return {u[(t + 2) % 3], u[t % 3], u[(t + 1) % 3], t - 1};
 }
 
-void enqueue_acoustic_step(Plan& p, int64_t k, float* const* u, bool stencil_only = false) {
+// The vector ring kernel carries the sparse work of single-domain 3D plans
+// when every injection cell lies in its tile grid (ensure_fused).
+bool fused_sparse_active(const Plan& p) {
+    return p.fused.ok && !p.fused_disabled && p.kind == Plan::ACOUSTIC && p.ndim == 3 &&
+           p.use_vec && !p.use_vecq && !p.slab && !p.nccl_comm;
+}
+
+// [first, last): the step range being enqueued (fused sampling lags one step)
+void enqueue_acoustic_step(Plan& p, int64_t k, float* const* u, bool stencil_only = false,
+                           int64_t first = 0, int64_t last = -1) {
     const StepSlots st = step_slots(p, k, u);
     const PointSet& inj = p.ac.forward ? p.src : p.rec;
     const PointSet& smp = p.ac.forward ? p.rec : p.src;
@@ -1054,6 +1131,20 @@ void enqueue_acoustic_step(Plan& p, int64_t k, float* const* u, bool stencil_onl
         launch_inject(p, inj, st.out, st.row, inj.nband0, inj.ncells - inj.nband0);
         SF_CUDA(cudaStreamWaitEvent(p.stream, p.ev_comm, 0));
         launch_sample(p, smp, st.out, st.row);
+        return;
+    }
+    if (!stencil_only && fused_sparse_active(p)) {
+        // one launch per step: injection of this step in the CTAs' epilogue,
+        // sampling of the previous step (k > first) from this step's cur
+        Epilogue epi;
+        epi.inj = &inj;
+        epi.inj_row = st.row;
+        if (k > first) {
+            epi.smp = &smp;
+            epi.smp_row = p.ac.forward ? st.row - 1 : st.row + 1;
+        }
+        launch_stencil(p, st.out, st.cur, st.prev, nullptr, nullptr, nullptr, &epi);
+        if (k + 1 == last) launch_sample(p, smp, st.out, st.row);
         return;
     }
     launch_stencil(p, st.out, st.cur, st.prev);
@@ -1299,14 +1390,99 @@ void enqueue_steps(Plan& p, int64_t b, int64_t e) {
         if (p.kind == Plan::DIFFUSION)
             enqueue_diffusion_step(p, k);
         else
-            enqueue_acoustic_step(p, k, p.slot);
+            enqueue_acoustic_step(p, k, p.slot, false, b, e);
     }
+}
+
+// Tile-sorted copy of the injection CSR for the fused epilogue: cells of
+// CTA b (launch order) in [tile_start[b], tile_start[b+1]), each cell's
+// contributions still in ascending point order. Rebuilt when the points or
+// the tile geometry change; not built (fused path off) when a cell lies
+// outside the planes / tiles the stencil kernel covers.
+void ensure_fused(Plan& p) {
+    if (p.fused_disabled || p.kind != Plan::ACOUSTIC || p.ndim != 3 || !p.use_vec || p.use_vecq ||
+        p.slab || p.nccl_comm) {
+        p.fused.ok = false;
+        return;
+    }
+    const PointSet& inj = p.ac.forward ? p.src : p.rec;
+    const int64_t tx = 32 * p.tile_nx, ty = 4 * p.vec_warps / p.tile_nx;
+    const uint64_t key[8] = {inj.version + 1, p.grid3.x, p.grid3.y, p.grid3.z,
+                             static_cast<uint64_t>(p.zchunk), static_cast<uint64_t>(tx),
+                             static_cast<uint64_t>(ty),
+                             (static_cast<uint64_t>(p.z0) << 32) | static_cast<uint32_t>(p.z1)};
+    if (std::memcmp(key, p.fused.key, sizeof key) == 0) return;
+    std::memcpy(p.fused.key, key, sizeof key);
+    clear_graphs(p);
+    p.fused.ok = false;
+    const int64_t gx = p.grid3.x, gy = p.grid3.y, gz = p.grid3.z;
+    const int64_t ntiles = gx * gy * gz;
+    const int nc = inj.ncells;
+    std::vector<int64_t> tile(static_cast<size_t>(nc));
+    for (int i = 0; i < nc; ++i) {
+        const int64_t off = inj.h_cells[i];
+        const int64_t a0 = off / p.plane, a1 = (off % p.plane) / p.pitch, a2 = off % p.pitch;
+        if (a0 < p.z0 || a0 >= p.z1 || a2 >= gx * tx || a1 >= gy * ty) return;
+        tile[i] = a2 / tx + gx * (a1 / ty + gy * ((a0 - p.z0) / p.zchunk));
+        if (tile[i] >= ntiles) return;
+    }
+    std::vector<int> order(static_cast<size_t>(nc));
+    for (int i = 0; i < nc; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return tile[a] < tile[b]; });
+    std::vector<int> tstart(static_cast<size_t>(ntiles + 1), 0);
+    std::vector<int64_t> cell;
+    std::vector<int> start, cp;
+    std::vector<float> cw;
+    for (int i = 0; i < nc; ++i) ++tstart[tile[i] + 1];
+    for (int64_t t = 0; t < ntiles; ++t) tstart[t + 1] += tstart[t];
+    for (int oi : order) {
+        cell.push_back(inj.h_cells[oi]);
+        start.push_back(static_cast<int>(cp.size()));
+        for (int j = inj.h_start[oi]; j < inj.h_start[oi + 1]; ++j) {
+            cp.push_back(inj.h_cp[j]);
+            cw.push_back(inj.h_cw[j]);
+        }
+    }
+    start.push_back(static_cast<int>(cp.size()));
+    if (cell.empty()) cell.push_back(0);
+    if (cp.empty()) {
+        cp.push_back(0);
+        cw.push_back(0.0f);
+    }
+    auto& f = p.fused;
+    if (static_cast<size_t>(ntiles + 1) > f.cap_tiles) {
+        dfree(f.tile_start);
+        f.cap_tiles = static_cast<size_t>(ntiles + 1);
+        f.tile_start = dalloc<int>(f.cap_tiles);
+    }
+    if (cell.size() > f.cap_cells) {
+        dfree(f.cell);
+        dfree(f.start);
+        f.cap_cells = cell.size();
+        f.cell = dalloc<int64_t>(f.cap_cells);
+        f.start = dalloc<int>(f.cap_cells + 1);
+    }
+    if (cp.size() > f.cap_contrib) {
+        dfree(f.cp);
+        dfree(f.cw);
+        f.cap_contrib = cp.size();
+        f.cp = dalloc<int>(f.cap_contrib);
+        f.cw = dalloc<float>(f.cap_contrib);
+    }
+    SF_CUDA(cudaStreamSynchronize(p.stream));
+    SF_CUDA(cudaMemcpy(f.tile_start, tstart.data(), tstart.size() * sizeof(int), cudaMemcpyHostToDevice));
+    SF_CUDA(cudaMemcpy(f.cell, cell.data(), cell.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    SF_CUDA(cudaMemcpy(f.start, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice));
+    SF_CUDA(cudaMemcpy(f.cp, cp.data(), cp.size() * sizeof(int), cudaMemcpyHostToDevice));
+    SF_CUDA(cudaMemcpy(f.cw, cw.data(), cw.size() * sizeof(float), cudaMemcpyHostToDevice));
+    f.ok = true;
 }
 
 // Steps [b, e) as one cached CUDA graph (the OpenMP team + barriers of the
 // generated loop become graph edges; launches cost ~graph-node latency).
 void run_steps(Plan& p, int64_t b, int64_t e) {
     if (b >= e && b >= 0) return;
+    if (b >= 0) ensure_fused(p);
     auto key = std::make_pair(b, e);
     auto it = p.graphs.find(key);
     if (it == p.graphs.end()) {
@@ -1460,6 +1636,7 @@ void choose_geometry(Plan& p) {
 // SF_NO_TMA=1 (per-thread loads only).
 void enable_tma(Plan& p) {
     if (p.ndim != 3) return;
+    if (const char* env = std::getenv("SF_NO_FUSED_SPARSE")) p.fused_disabled = env[0] == '1';
     if (const char* env = std::getenv("SF_NO_TMA"))
         if (env[0] == '1') return;
     const char* vec = std::getenv("SF_VEC");
@@ -2328,7 +2505,8 @@ int sf_plan_time(sf_plan* p, float* total_ms, float* stencil_ms, int64_t* launch
         if (total_ms) *total_ms = ms;
         if (launches)
             *launches = p->kind == sf_plan::DIFFUSION ? sfb::diffusion_launches(*p, p->nt)
-                                                      : sfb::launches_per_step_of(*p) * p->nt;
+                                                      : sfb::launches_per_step_of(*p) * p->nt +
+                                                            (sfb::fused_sparse_active(*p) ? 1 : 0);
         if (stencil_ms) {
             // same steps with only the stencil launches: their summed duration
             sfb::run_steps(*p, sfb::kStencilOnly, sfb::kStencilOnly);

@@ -53,6 +53,24 @@ struct TmaStencilArgs {
     float tc[3];
     float c0;
     float cj[8];
+    // Fused sparse epilogue (vector ring kernel): after its last plane a CTA
+    // (1) injects this step's sources into the cells of its own tile (a
+    // tile-sorted copy of the injection CSR: cells [tile_start[b],
+    // tile_start[b+1]) belong to CTA b) and (2) samples the PREVIOUS step's
+    // receivers from `cur`, which this step does not write. Null / 0 = off.
+    const int* inj_tile_start;
+    const int64_t* inj_cell;
+    const int* inj_start;
+    const int* inj_cp;
+    const float* inj_cw;
+    const float* inj_row;  // series row of this step
+    const float* mfield;   // m (the injection divides by it)
+    float inj_scale;
+    const float* smp_field;
+    const int* smp_ci;
+    const float* smp_w;
+    float* smp_out;        // series row of the previous step
+    int smp_np;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
