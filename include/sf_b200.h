@@ -224,6 +224,11 @@ int sf_plan_autotune(sf_plan *plan, int64_t tune_steps, int repeats, sf_tune_ent
 int sf_diffusion_constants(int order, int64_t alpha_num, int64_t alpha_den, int64_t dx_num,
                            int64_t dx_den, float *c0, int *has_c0, float *cj /* [8] */);
 
+/* Self-test of the stencil kernels' reciprocal (1.0f / x, exact IEEE
+ * round-to-nearest via MUFU.RCP + one Newton step with a slow-path guard)
+ * against __frcp_rn over all 2^32 float bit patterns; *mismatches = count. */
+int sf_selftest_reciprocal(int device, unsigned long long *mismatches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -2226,6 +2226,22 @@ extern "C" int sf_plan_save_series_text(sf_plan* p, const char* name, const char
     });
 }
 
+extern "C" int sf_selftest_reciprocal(int device, unsigned long long* mismatches) {
+    using namespace sfb;
+    if (!mismatches) return SF_ERR_INVALID;
+    return guard([&] {
+        SF_CUDA(cudaSetDevice(device));
+        unsigned long long* d = dalloc<unsigned long long>(1);
+        SF_CUDA(cudaMemset(d, 0, sizeof(unsigned long long)));
+        const uint32_t chunk = 1u << 30;  // float bit patterns per launch
+        for (uint64_t first = 0; first < (1ull << 32); first += chunk)
+            rcp4_check_kernel<<<chunk / 4 / 256, 256>>>(static_cast<uint32_t>(first), chunk, d);
+        SF_CUDA(cudaGetLastError());
+        SF_CUDA(cudaMemcpy(mismatches, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        dfree(d);
+    });
+}
+
 extern "C" {
 
 const char* sf_last_error(void) { return sfb::g_error.c_str(); }

@@ -441,3 +441,12 @@ def test_text_dumps_match_reference(sf, ref, tmp_path):
         s3.op.dump_csv("u", tmp_path / "bad3d.csv", 0)   # 2D grids only
     with pytest.raises(sf.SfError):
         s3.op.save_series_text("m", tmp_path / "bad.txt")
+
+
+def test_reciprocal_exact_on_every_float(sf):
+    """The stencil kernels' batched reciprocal (fast path + guarded library
+    fallback) equals __frcp_rn == __fdiv_rn(1, x) on all 2^32 inputs."""
+    import ctypes as C
+    bad = C.c_ulonglong(123)
+    assert sf._lib.lib.sf_selftest_reciprocal(0, C.byref(bad)) == 0, sf._lib.last_error()
+    assert bad.value == 0
