@@ -94,6 +94,21 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 // instead of re-issuing the poll: spinning waiters otherwise take issue slots
 // from the compute warps of the same scheduler. Bounded: a wait that never
 // completes (a TMA fault, a mis-sized box) traps instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait_addr(uint32_t addr, uint32_t parity) {
+    uint32_t done = 0;
+    for (uint32_t spins = 0;; ++spins) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity), "r"(20000u)
+            : "memory");
+        if (done) return;
+        if (spins > (1u << 22)) __trap();
+    }
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t done = 0;
     for (uint32_t spins = 0;; ++spins) {
