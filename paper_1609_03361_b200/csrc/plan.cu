@@ -1535,6 +1535,10 @@ void chunk_grid(const Plan& p, int64_t wx, int64_t wy, int per_sm, dim3* grid, i
             best_gz = gz;
         }
     }
+    if (const char* env = std::getenv("SF_ZCHUNKS")) {  // experiments: force the chunk count
+        const int64_t v = std::atoll(env);
+        if (v >= 1 && v <= nz) best_gz = v;
+    }
     const int64_t zc = (nz + best_gz - 1) / best_gz;
     *zchunk = static_cast<int>(zc);
     *grid = dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy),
