@@ -313,7 +313,9 @@ def run_reference_arm(args, world, rank):
     line = {
         "impl": "reference", "metric": "GPts/s (grid-point updates/sec)", "value": base["value"],
         "unit": "GPts/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        # one bench step = one full apply (all nt time steps) at the sampled rate
+        "ms_per_step": interior_points(model) * model.nt / (base["value"] * 1e9) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
         "config": config_block(args, model),
         "cpu_baseline": base,
