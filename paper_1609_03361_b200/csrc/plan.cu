@@ -550,18 +550,45 @@ void launch_vec_grad(int r, dim3 g, size_t smem, cudaStream_t st, const TmaStenc
     }
 }
 
+// Programmatic dependent launch: a vector-kernel launch may begin while the
+// previous kernel on the stream drains (its CTAs prefetch the static m/eta
+// boxes, then griddepcontrol.wait for the previous grid before touching
+// anything it wrote). SF_NO_PDL=1 launches plainly.
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SF_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
+template <typename Kern>
+void launch_pdl(Kern kernel, dim3 g, dim3 b, size_t smem, cudaStream_t st, const TmaStencilArgs& A) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    SF_CUDA(cudaLaunchKernelEx(&cfg, kernel, A));
+}
+
 template <bool FWD>
 void launch_vec(int r, int warps, int nx, dim3 g, size_t smem, cudaStream_t st,
                 const TmaStencilArgs& A) {
     const dim3 b(32 * (warps + 1));  // + the TMA producer warp
-#define SF_V(RR)                                                                   \
-    case RR:                                                                       \
-        if (nx == 1)                                                               \
-            acoustic3d_vec_kernel<RR, FWD, 4, false, 8><<<g, b, smem, st>>>(A);    \
-        else if (warps == 4)                                                       \
-            acoustic3d_vec_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);              \
-        else                                                                       \
-            acoustic3d_vec_kernel<RR, FWD, 8><<<g, b, smem, st>>>(A);              \
+#define SF_V(RR)                                                                         \
+    case RR:                                                                             \
+        if (nx == 1)                                                                     \
+            launch_pdl(acoustic3d_vec_kernel<RR, FWD, 4, false, 8>, g, b, smem, st, A);  \
+        else if (warps == 4)                                                             \
+            launch_pdl(acoustic3d_vec_kernel<RR, FWD, 4>, g, b, smem, st, A);            \
+        else                                                                             \
+            launch_pdl(acoustic3d_vec_kernel<RR, FWD, 8>, g, b, smem, st, A);            \
         return;
     switch (r) {
         SF_V(1) SF_V(2) SF_V(3) SF_V(4)
