@@ -381,7 +381,8 @@ def run_b200_arm(args, world, rank, local):
             traffic = None
     # e2e through the C-ABI apply with pinned host buffers
     h2d = sum(a.data.nbytes for a in op.args)
-    d2h = setup.field.data.nbytes + setup.src.data.data.nbytes + setup.rec.data.data.nbytes
+    # apply returns what the kernel writes: the three slots and the receiver traces
+    d2h = setup.field.data.nbytes + setup.rec.data.data.nbytes
     op.apply()  # warm
     barrier(world)
     t0 = time.perf_counter()
@@ -651,7 +652,7 @@ def run_b200_slabs(args, world, rank, local):
         sf.api.check(_lib.lib.sf_plan_invoke(slab.plan, argv, 9))
     e2e_s = max_over_ranks(world, (time.perf_counter() - t_e) / args.steps)
     h2d = sum(b.nbytes for b in slab.bufs)
-    d2h = slab.bufs[0].nbytes + slab.bufs[3].nbytes + slab.bufs[6].nbytes
+    d2h = slab.bufs[0].nbytes + slab.bufs[6].nbytes
     if rank == 0:
         line = {
             "metric": "GPts/s (grid-point updates/sec)", "value": value, "unit": "GPts/s",

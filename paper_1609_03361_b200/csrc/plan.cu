@@ -2514,7 +2514,14 @@ int sf_plan_invoke(sf_plan* p, void* const* args, int nargs) {
         sfb::upload_any(*p, args, nargs);
         sfb::run_steps(*p, 0, p->nt);
         sfb::check_kernel_errors(*p);
-        sfb::download_any(*p, args, nargs);
+        // only what the kernel writes comes back (the generated Operator
+        // stores into the field and the sampled series; m, eta, the injected
+        // series, ci and w are read-only, so the host copies already match)
+        std::vector<void*> out(args, args + nargs);
+        if (p->kind == sf_plan::ACOUSTIC)
+            for (int i = 1; i < nargs; ++i)
+                if (i != (p->ac.forward ? 6 : 3)) out[i] = nullptr;
+        sfb::download_any(*p, out.data(), nargs);
     });
 }
 
