@@ -232,6 +232,10 @@ def max_over_ranks(world, value):
 def cpu_reference_sample(model, cfg_name, v_field, v_min, steps=1, warmup=1, budget_s=20.0):
     """The reference's CPU path (oracle/_ref: stencilforge JIT kernel) on a
     bounded sample: the full grid for nt_s time steps. Returns GPts/s."""
+    # SURVEY 8(d) CPU protocol: all host threads, pinned close to cores
+    # (read by libgomp when the reference library loads it)
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_lib as ol
     if ol.have_ref():
@@ -283,7 +287,8 @@ def cpu_reference_sample(model, cfg_name, v_field, v_min, steps=1, warmup=1, bud
     gpts = interior_points(model) * nt_s / secs / 1e9
     sample = (f"{cfg_name} grid {'x'.join(map(str, model.shape))} order {model.space_order}, "
               f"{nt_s} of {model.nt} time steps, median of {max(1, steps)} applies after "
-              f"{warmup} warm-up, JIT excluded")
+              f"{warmup} warm-up, JIT excluded, OMP_PROC_BIND={os.environ.get('OMP_PROC_BIND')} "
+              f"OMP_PLACES={os.environ.get('OMP_PLACES')}")
     return {"value": gpts, "unit": "GPts/s", "cores": threads, "kind": kind, "sample": sample}
 
 
