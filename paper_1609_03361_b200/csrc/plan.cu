@@ -1913,6 +1913,11 @@ sf_plan::~sf_plan() {
     sfb::dfree(eta);
     sfb::free_points(src);
     sfb::free_points(rec);
+    sfb::dfree(fused.tile_start);
+    sfb::dfree(fused.cell);
+    sfb::dfree(fused.start);
+    sfb::dfree(fused.cp);
+    sfb::dfree(fused.cw);
     sfb::dfree(hist);
     sfb::dfree(grad);
     for (float* s : v) sfb::dfree(s);
