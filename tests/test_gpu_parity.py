@@ -450,3 +450,71 @@ def test_reciprocal_exact_on_every_float(sf):
     bad = C.c_ulonglong(123)
     assert sf._lib.lib.sf_selftest_reciprocal(0, C.byref(bad)) == 0, sf._lib.last_error()
     assert bad.value == 0
+
+
+@pytest.mark.parametrize("order,shape", [(4, (30, 41, 75)), (4, (26, 38, 101)), (8, (34, 40, 70)),
+                                         (2, (22, 27, 45))])
+@pytest.mark.parametrize("forward", [True, False])
+@pytest.mark.parametrize("split", [None, (1, 5), (3, 4, 9)])
+def test_step_ranges_and_tile_edge_points(sf, port, order, shape, forward, split):
+    """The fused sparse epilogue (injection per CTA tile, sampling one step
+    late) under every way of cutting [0, nt) into sf_plan_run ranges, with
+    points on tile edges, sharing cells, and one in the non-interior shell
+    (which turns the fused path off for the plan)."""
+    import ctypes as C
+    from paper_1609_03361_b200 import _lib
+    nt = 11
+    r = order // 2
+    h = 10.0
+    rng = np.random.default_rng(order * 100 + shape[2] + int(forward))
+    v = 1500.0 + 3000.0 * rng.random(shape)
+    m, eta = port.medium_from_velocity(v, 4, h, 1500.0)
+    dt = min(0.4 * h / 4500.0, port.stable_dt(3, order, h, 4500.0, 4500.0))
+    # cells on 32- and 64-wide tile edges in a2, 8/16-row edges in a1, chunk
+    # edges in a0, a shared cell, plus (maybe) one point in the outer shell
+    cells = [(r + 1, 15.5, 31.5), (shape[0] // 2, 16.0, 32.0), (shape[0] - r - 2, 7.5, 63.5),
+             (r + 3, 8.2, 31.9), (r + 3, 8.2, 31.9)]
+    inner = [[a0 * h, a1 * h, min(a2, shape[2] - r - 2.5) * h] for a0, a1, a2 in cells]
+    rec_c = np.concatenate([inner, np.stack([rng.uniform((r + 1) * h, (e - r - 2) * h, 37)
+                                             for e in shape], 1)])
+    src_c = np.array(inner[:4] + ([[0.3 * h, 9.0 * h, 9.0 * h]] if split == (1, 5) else []))
+    src_ci, src_w = port.interp(src_c, h, shape)
+    rec_ci, rec_w = port.interp(rec_c, h, shape)
+    ns, nr = len(src_ci), len(rec_ci)
+    u0 = (1e-3 * rng.standard_normal((3,) + shape)).astype(np.float32)
+    if forward:
+        src = rng.standard_normal((nt, ns)).astype(np.float32)
+        rec = np.zeros((nt, nr), np.float32)
+    else:
+        src = np.zeros((nt, ns), np.float32)
+        rec = rng.standard_normal((nt, nr)).astype(np.float32)
+    # oracle
+    coefs = port.coefs(3, order, forward, dt, h)
+    want_u, want_src, want_rec = u0.copy(), src.copy(), rec.copy()
+    if forward:
+        port.acoustic_run(coefs, want_u, m, eta, want_src, src_ci, src_w, want_rec, rec_ci, rec_w, nt)
+    else:
+        port.acoustic_run(coefs, want_u, m, eta, want_rec, rec_ci, rec_w, want_src, src_ci, src_w,
+                          nt)
+    # GPU, in pieces
+    d = _lib.AcousticDesc()
+    d.ndim = 3
+    for i, e in enumerate(shape):
+        d.shape[i] = e
+    d.space_order, d.forward, d.nt, d.dt, d.spacing = order, int(forward), nt, dt, h
+    d.n_src, d.n_rec = ns, nr
+    plan = C.c_void_p()
+    sf.api.check(_lib.lib.sf_acoustic_plan_create(C.byref(d), 0, C.byref(plan)))
+    try:
+        bufs = [np.ascontiguousarray(b) for b in
+                (u0.copy(), m, eta, src.copy(), src_ci, src_w, rec.copy(), rec_ci, rec_w)]
+        argv = (C.c_void_p * 9)(*[b.ctypes.data for b in bufs])
+        sf.api.check(_lib.lib.sf_plan_upload(plan, argv, 9))
+        edges = [0] + list(split or []) + [nt]
+        for a, b in zip(edges[:-1], edges[1:]):
+            sf.api.check(_lib.lib.sf_plan_run(plan, a, b))
+        sf.api.check(_lib.lib.sf_plan_download(plan, argv, 9))
+    finally:
+        _lib.lib.sf_plan_destroy(plan)
+    assert_parity(bufs[0], want_u)
+    assert_parity(bufs[6] if forward else bufs[3], want_rec if forward else want_src)
