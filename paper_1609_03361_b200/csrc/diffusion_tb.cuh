@@ -103,7 +103,11 @@ __global__ void __launch_bounds__(256) diffusion_tb_kernel(const __grid_constant
     // (4 + 2RA)-float window (LDS.128s) gives every a1 neighbour, one
     // LDS.128 per a0 row offset gives the a0 neighbours of all four.
     constexpr int RA = (R + 3) / 4 * 4;
-    const int lx = tid & 15, ly = tid >> 4;  // 16 vectors x 16 rows per pass
+    // a pass covers whole smem rows: NV float4 columns x RPP rows (the
+    // 66-78 wide valid region would leave most of a second 64-wide pass idle)
+    constexpr int NV = SW / 4;
+    constexpr int RPP = 256 / NV;
+    const int lx = tid % NV, ly = tid / NV;
     for (int st = 1; st <= T; ++st) {
         const float* in = sbuf + ((st - 1) & 1) * (SW * SW);
         float* out = sbuf + (st & 1) * (SW * SW);
@@ -114,8 +118,10 @@ __global__ void __launch_bounds__(256) diffusion_tb_kernel(const __grid_constant
         const int ix0 = R - gx0, ix1 = A.n1 - R - gx0;
         const int ylo = max(grow, iy0), yhi = min(SW - grow, iy1);
         const int xlo = max(grow, ix0) & ~3, xhi = min(SW - grow, ix1);
-        for (int y = ylo + ly; y < yhi; y += 16) {
-            for (int x = xlo + 4 * lx; x < xhi; x += 64) {
+        const int x = 4 * lx;
+        const bool col_on = ly < RPP && x + 3 >= xlo && x < xhi;
+        for (int y = ylo + ly; col_on && y < yhi; y += RPP) {
+            {
                 const float* c = in + y * SW + x;
                 float win[4 + 2 * RA];
 #pragma unroll
