@@ -1124,8 +1124,8 @@ StepSlots step_slots(const Plan& p, int64_t k, float* const* u) {
 // The vector ring kernel carries the sparse work of single-domain 3D plans
 // when every injection cell lies in its tile grid (ensure_fused).
 bool fused_sparse_active(const Plan& p) {
-    return p.fused.ok && !p.fused_disabled && p.kind == Plan::ACOUSTIC && p.ndim == 3 &&
-           p.use_vec && !p.use_vecq && !p.slab && !p.nccl_comm;
+    return p.fused.ok && !p.fused_disabled && (p.kind == Plan::ACOUSTIC || p.kind == Plan::FWI) &&
+           p.ndim == 3 && p.use_vec && !p.use_vecq && !p.slab && !p.nccl_comm;
 }
 
 // [first, last): the step range being enqueued (fused sampling lags one step)
@@ -1361,8 +1361,22 @@ void enqueue_fwi_forward(Plan& p) {
     p.ac = p.ac_fwd;
     const int64_t L = p.slot_elems;
     SF_CUDA(cudaMemsetAsync(p.hist, 0, sizeof(float) * 2 * L, p.stream));
+    const bool fused = fused_sparse_active(p);
     for (int64_t t = 0; t < p.nt; ++t) {
         float* out = p.hist + (t + 2) * L;
+        if (fused) {  // injection of step t, sampling of step t-1 in the epilogue
+            Epilogue epi;
+            epi.inj = &p.src;
+            epi.inj_row = t;
+            if (t > 0) {
+                epi.smp = &p.rec;
+                epi.smp_row = t - 1;
+            }
+            launch_stencil(p, out, p.hist + (t + 1) * L, p.hist + t * L, nullptr, nullptr, nullptr,
+                           &epi);
+            if (t + 1 == p.nt) launch_sample(p, p.rec, out, t);
+            continue;
+        }
         launch_stencil(p, out, p.hist + (t + 1) * L, p.hist + t * L);
         launch_inject_sample(p, p.src, p.rec, out, t);
     }
@@ -1427,8 +1441,9 @@ void enqueue_steps(Plan& p, int64_t b, int64_t e) {
 // the tile geometry change; not built (fused path off) when a cell lies
 // outside the planes / tiles the stencil kernel covers.
 void ensure_fused(Plan& p) {
-    if (p.fused_disabled || p.kind != Plan::ACOUSTIC || p.ndim != 3 || !p.use_vec || p.use_vecq ||
-        p.slab || p.nccl_comm) {
+    // FWI: the forward sweep (p.ac is the forward set outside the adjoint)
+    if (p.fused_disabled || (p.kind != Plan::ACOUSTIC && p.kind != Plan::FWI) || p.ndim != 3 ||
+        !p.use_vec || p.use_vecq || p.slab || p.nccl_comm) {
         p.fused.ok = false;
         return;
     }
@@ -1509,7 +1524,7 @@ void ensure_fused(Plan& p) {
 // generated loop become graph edges; launches cost ~graph-node latency).
 void run_steps(Plan& p, int64_t b, int64_t e) {
     if (b >= e && b >= 0) return;
-    if (b >= 0) ensure_fused(p);
+    if (b >= 0 || b == kFwiForward) ensure_fused(p);
     auto key = std::make_pair(b, e);
     auto it = p.graphs.find(key);
     if (it == p.graphs.end()) {
