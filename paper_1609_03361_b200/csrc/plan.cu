@@ -130,6 +130,7 @@ struct sf_plan {
     bool use_vec = false;  // 4 points/thread, LDS.128 variant of the TMA pipeline
     bool use_vecq = false; // ... with the a0 neighbours in a register queue (radius >= 5)
     int vec_warps = 8;
+    int vec_rpl = 1;  // vector kernel: rows of four points per lane (1 or 2)
     int tma_stages = 4;
     int stages_override = 0;  // autotune: > 0 forces the pipeline depth
     size_t tma_smem = 0;
@@ -463,27 +464,38 @@ size_t tma_smem_bytes(int r, int nx, int stages) {
 
 // ---- vectorised TMA path (4 consecutive a2 points per thread) -------------
 // tile_nx selects the tile width for the vector kernel: 2 -> 64-wide tiles
-// (16 lanes per row), 1 -> 32-wide (8 lanes per row, 4-warp CTAs only)
-template <bool FWD>
-const void* vec_ptr(int r, int warps, int nx = 2) {
-#define SF_V(RR)                                                                              \
-    case RR:                                                                                  \
-        if (nx == 1)                                                                          \
-            return warps == 4 ? reinterpret_cast<const void*>(                                \
-                                    &acoustic3d_vec_kernel<RR, FWD, 4, false, 8>)             \
-                              : nullptr;                                                      \
-        return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4>) \
-                          : reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 8>);
-    switch (r) {
-        SF_V(1) SF_V(2) SF_V(3) SF_V(4)
-        default: return nullptr;
+// (16 lanes per row), 1 -> 32-wide (8 lanes per row); rpl = rows per lane.
+// Compiled shapes (warps, nx, rpl): (4,2,1) (8,2,1) (4,1,1) (2,1,2) (4,2,2).
+template <bool FWD, int RR>
+const void* vec_ptr_r(int warps, int nx, int rpl) {
+    if (rpl == 2) {
+        if (nx == 1 && warps == 2)
+            return reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 2, false, 8, 2>);
+        if (nx == 2 && warps == 4)
+            return reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4, false, 16, 2>);
+        return nullptr;
     }
-#undef SF_V
+    if (nx == 1)
+        return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4, false, 8>)
+                          : nullptr;
+    return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4>)
+                      : reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 8>);
 }
 
-size_t vec_smem_bytes(int r, int warps, int stages, int npme = 3, int nx = 2) {
+template <bool FWD>
+const void* vec_ptr(int r, int warps, int nx = 2, int rpl = 1) {
+    switch (r) {
+        case 1: return vec_ptr_r<FWD, 1>(warps, nx, rpl);
+        case 2: return vec_ptr_r<FWD, 2>(warps, nx, rpl);
+        case 3: return vec_ptr_r<FWD, 3>(warps, nx, rpl);
+        case 4: return vec_ptr_r<FWD, 4>(warps, nx, rpl);
+        default: return nullptr;
+    }
+}
+
+size_t vec_smem_bytes(int r, int warps, int stages, int npme = 3, int nx = 2, int rpl = 1) {
     const int ra = (r + 3) / 4 * 4;
-    const int tx = 32 * nx, ty = 4 * warps / nx;
+    const int tx = 32 * nx, ty = 4 * warps * rpl / nx;
     const int wb = tx + 2 * ra, h = ty + 2 * r;
     const int cur = (wb * h * 4 + 127) / 128 * 128;
     const int pme = (tx * ty * 4 + 127) / 128 * 128;
@@ -578,17 +590,21 @@ void launch_pdl(Kern kernel, dim3 g, dim3 b, size_t smem, cudaStream_t st, const
 }
 
 template <bool FWD>
-void launch_vec(int r, int warps, int nx, dim3 g, size_t smem, cudaStream_t st,
+void launch_vec(int r, int warps, int nx, int rpl, dim3 g, size_t smem, cudaStream_t st,
                 const TmaStencilArgs& A) {
     const dim3 b(32 * (warps + 1));  // + the TMA producer warp
-#define SF_V(RR)                                                                         \
-    case RR:                                                                             \
-        if (nx == 1)                                                                     \
-            launch_pdl(acoustic3d_vec_kernel<RR, FWD, 4, false, 8>, g, b, smem, st, A);  \
-        else if (warps == 4)                                                             \
-            launch_pdl(acoustic3d_vec_kernel<RR, FWD, 4>, g, b, smem, st, A);            \
-        else                                                                             \
-            launch_pdl(acoustic3d_vec_kernel<RR, FWD, 8>, g, b, smem, st, A);            \
+#define SF_V(RR)                                                                             \
+    case RR:                                                                                 \
+        if (rpl == 2 && nx == 1)                                                             \
+            launch_pdl(acoustic3d_vec_kernel<RR, FWD, 2, false, 8, 2>, g, b, smem, st, A);   \
+        else if (rpl == 2)                                                                   \
+            launch_pdl(acoustic3d_vec_kernel<RR, FWD, 4, false, 16, 2>, g, b, smem, st, A);  \
+        else if (nx == 1)                                                                    \
+            launch_pdl(acoustic3d_vec_kernel<RR, FWD, 4, false, 8>, g, b, smem, st, A);      \
+        else if (warps == 4)                                                                 \
+            launch_pdl(acoustic3d_vec_kernel<RR, FWD, 4>, g, b, smem, st, A);                \
+        else                                                                                 \
+            launch_pdl(acoustic3d_vec_kernel<RR, FWD, 8>, g, b, smem, st, A);                \
         return;
     switch (r) {
         SF_V(1) SF_V(2) SF_V(3) SF_V(4)
@@ -640,7 +656,8 @@ void setup_tma(Plan& p) {
     const int vnx = p.use_vecq ? 2 : nx;
     const uint32_t wb = static_cast<uint32_t>(p.use_vec ? 32 * vnx + 2 * ((r + 3) / 4 * 4)
                                                         : tma_box_width(r, nx));
-    const uint32_t ty = static_cast<uint32_t>(p.use_vec ? 4 * p.vec_warps / vnx : 8);
+    const uint32_t ty = static_cast<uint32_t>(
+        p.use_vec ? 4 * p.vec_warps * (p.use_vecq ? 1 : p.vec_rpl) / vnx : 8);
     const uint32_t tx = static_cast<uint32_t>(p.use_vec ? 32 * vnx : 32 * nx);
     const uint32_t cy = ty + static_cast<uint32_t>(2 * r);
     for (int s = 0; s < 3; ++s) {
@@ -678,16 +695,19 @@ void setup_tma(Plan& p) {
     }
     if (p.use_vec) {
         int stages = 3;
-        while (stages > 2 && vec_smem_bytes(r, p.vec_warps, stages, 3, nx) * 2 > 226 * 1024) --stages;
+        const int rpl = p.vec_rpl;
+        while (stages > 2 && vec_smem_bytes(r, p.vec_warps, stages, 3, nx, rpl) * 2 > 226 * 1024)
+            --stages;
         if (const char* env = std::getenv("SF_TMA_STAGES")) {
             const int v = std::atoi(env);
             if (v >= 2 && v <= 16) stages = v;
         }
         if (p.stages_override >= 2) stages = p.stages_override;
         p.tma_stages = stages;
-        p.tma_smem = vec_smem_bytes(r, p.vec_warps, stages, 3, nx);
+        p.tma_smem = vec_smem_bytes(r, p.vec_warps, stages, 3, nx, rpl);
         for (int fwd = 0; fwd < 2; ++fwd) {
-            const void* fn = fwd ? vec_ptr<true>(r, p.vec_warps, nx) : vec_ptr<false>(r, p.vec_warps, nx);
+            const void* fn = fwd ? vec_ptr<true>(r, p.vec_warps, nx, rpl)
+                                 : vec_ptr<false>(r, p.vec_warps, nx, rpl);
             if (!fn) throw Status(SF_ERR_INVALID, "vector stencil not compiled");
             SF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(p.tma_smem)));
@@ -907,9 +927,11 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
                 T.smp_np = static_cast<int>(epi->smp->np);
             }
             if (p.ac.forward)
-                launch_vec<true>(p.ac.radius, p.vec_warps, p.tile_nx, grid3, p.tma_smem, p.stream, T);
+                launch_vec<true>(p.ac.radius, p.vec_warps, p.tile_nx, p.vec_rpl, grid3, p.tma_smem,
+                                 p.stream, T);
             else
-                launch_vec<false>(p.ac.radius, p.vec_warps, p.tile_nx, grid3, p.tma_smem, p.stream, T);
+                launch_vec<false>(p.ac.radius, p.vec_warps, p.tile_nx, p.vec_rpl, grid3, p.tma_smem,
+                                  p.stream, T);
             return;
         }
         if (p.ac.forward)
@@ -1448,7 +1470,7 @@ void ensure_fused(Plan& p) {
         return;
     }
     const PointSet& inj = p.ac.forward ? p.src : p.rec;
-    const int64_t tx = 32 * p.tile_nx, ty = 4 * p.vec_warps / p.tile_nx;
+    const int64_t tx = 32 * p.tile_nx, ty = 4 * p.vec_warps * p.vec_rpl / p.tile_nx;
     const uint64_t key[8] = {inj.version + 1, p.grid3.x, p.grid3.y, p.grid3.z,
                              static_cast<uint64_t>(p.zchunk), static_cast<uint64_t>(tx),
                              static_cast<uint64_t>(ty),
@@ -1590,16 +1612,17 @@ void chunk_grid(const Plan& p, int64_t wx, int64_t wy, int per_sm, dim3* grid, i
 void set_grid(Plan& p) {
     const int r = p.ac.radius;
     const int64_t wx = p.use_vecq ? 64 : 32 * p.tile_nx;
-    const int64_t wy = p.use_vecq ? 2 * p.vec_warps : p.use_vec ? 4 * p.vec_warps / p.tile_nx
-                                                                 : p.tile_ty;
+    const int64_t wy = p.use_vecq ? 2 * p.vec_warps
+                       : p.use_vec ? 4 * p.vec_warps * p.vec_rpl / p.tile_nx
+                                   : p.tile_ty;
     int per_sm = 0;
     if (p.use_vecq) {
         const void* fn = p.ac.forward ? vecq_ptr<true>(r, p.vec_warps) : vecq_ptr<false>(r, p.vec_warps);
         if (fn)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.vec_warps, p.tma_smem);
     } else if (p.use_vec) {
-        const void* fn = p.ac.forward ? vec_ptr<true>(r, p.vec_warps, p.tile_nx)
-                                      : vec_ptr<false>(r, p.vec_warps, p.tile_nx);
+        const void* fn = p.ac.forward ? vec_ptr<true>(r, p.vec_warps, p.tile_nx, p.vec_rpl)
+                                      : vec_ptr<false>(r, p.vec_warps, p.tile_nx, p.vec_rpl);
         if (fn)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * (p.vec_warps + 1),
                                                           p.tma_smem);
@@ -1711,6 +1734,13 @@ void enable_tma(Plan& p) {
                 p.tile_nx = std::atoi(e) == 1 ? 1 : 2;
                 if (p.tile_nx == 1) p.vec_warps = 4;
             }
+            // two rows per lane: same tile, half the consumer warps
+            p.vec_rpl = 1;
+            if (const char* e = std::getenv("SF_VEC_RPL"))
+                if (std::atoi(e) == 2 && (p.tile_nx == 1 || p.vec_warps == 8)) {
+                    p.vec_rpl = 2;
+                    p.vec_warps = p.tile_nx == 1 ? 2 : 4;
+                }
         }
         setup_tma(p);
         p.use_tma = true;
@@ -1977,6 +2007,8 @@ void apply_config(Plan& p, const StencilConfig& c) {
     p.tile_nx = c.tile_nx;
     p.tile_ty = c.tile_ty;
     p.vec_warps = c.vec_warps;
+    // vector ring: tile_ty = 4 * warps * rows-per-lane / tile_nx
+    p.vec_rpl = c.kind == 2 ? std::max(1, c.tile_ty * c.tile_nx / (4 * c.vec_warps)) : 1;
     p.stages_override = c.stages;
     if (c.kind >= 1) {
         p.use_vec = c.kind >= 2;
@@ -1988,7 +2020,9 @@ void apply_config(Plan& p, const StencilConfig& c) {
 }
 
 StencilConfig current_config(const Plan& p) {
-    return {p.use_vecq ? 3 : p.use_vec ? 2 : p.use_tma ? 1 : 0, p.tile_nx, p.tile_ty, p.vec_warps,
+    const bool ring = p.use_vec && !p.use_vecq;
+    return {p.use_vecq ? 3 : p.use_vec ? 2 : p.use_tma ? 1 : 0, p.tile_nx,
+            ring ? 4 * p.vec_warps * p.vec_rpl / p.tile_nx : p.tile_ty, p.vec_warps,
             p.use_tma ? p.tma_stages : 0};
 }
 
@@ -2004,6 +2038,8 @@ std::vector<StencilConfig> tune_candidates(const Plan& p) {
         for (int w : {4, 8})
             for (int st : {2, 3, 4}) out.push_back({2, 2, 2 * w, w, st});
         for (int st : {2, 3, 4}) out.push_back({2, 1, 16, 4, st});
+        for (int st : {2, 3, 4}) out.push_back({2, 1, 16, 2, st});  // 2 rows per lane
+        for (int st : {2, 3}) out.push_back({2, 2, 16, 4, st});     // 2 rows per lane
     }
     if (r >= 5)
         for (int w : {4, 8})

@@ -312,7 +312,9 @@ def test_diffusion_temporal_blocking_vs_oracle(sf, port, order, n, nt):
 VARIANTS = [{}, {"SF_VEC": "0"}, {"SF_NO_TMA": "1"}, {"SF_VEC": "0", "SF_TMA": "1"},
             {"SF_VECQ": "0"}, {"SF_VEC_WARPS": "8"}, {"SF_TMA_STAGES": "2"},
             {"SF_VEC": "0", "SF_NO_TMA": "1", "SF_TILE": "2,16"}, {"SF_VEC_NX": "1"},
-            {"SF_VEC_NX": "1", "SF_TMA_STAGES": "4"}, {"SF_NO_FUSED_SPARSE": "1"}]
+            {"SF_VEC_NX": "1", "SF_TMA_STAGES": "4"}, {"SF_NO_FUSED_SPARSE": "1"},
+            {"SF_VEC_RPL": "2"}, {"SF_VEC_RPL": "2", "SF_VEC_NX": "1"},
+            {"SF_VEC_RPL": "2", "SF_VEC_NX": "2", "SF_VEC_WARPS": "8"}]
 
 
 @pytest.mark.parametrize("order", [2, 6, 8, 12])
