@@ -650,6 +650,7 @@ def run_b200_slabs(args, world, rank, local):
         slab.run(0, model.nt)
     barrier(world)
     tot = C.c_float()
+    sten = C.c_float()
     nl = C.c_int64()
     with ClockSampler(local) as clocks:
         total = 0.0
@@ -658,6 +659,9 @@ def run_b200_slabs(args, world, rank, local):
             total += tot.value
     barrier(world)
     ms_per_step = max_over_ranks(world, total / args.steps)
+    # per-rank stencil-only pass (no exchange) for the roofline of the kernel
+    sf.api.check(_lib.lib.sf_plan_time(slab.plan, C.byref(tot), C.byref(sten), C.byref(nl)))
+    sten_ms = max_over_ranks(world, sten.value)
     pts = 1
     for e in gshape:
         pts *= e - 2 * r
@@ -688,6 +692,14 @@ def run_b200_slabs(args, world, rank, local):
             "gpu_launches": int(nl.value * args.steps),
             "clocks": clocks.summary(),
         }
+        peak, peak_kind = load_peaks()
+        own_pts = pts // world  # each rank updates its own slab's interior share
+        achieved = 20 * own_pts / (sten_ms / model.nt / 1e3) / 1e9
+        line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                            "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                            "kernel": f"3D stencil (radius {r}) per rank, avg launch "
+                                      f"{sten_ms / model.nt * 1e3:.1f} us (stencil-only pass)",
+                            "alg_bytes_per_launch": 20 * own_pts}
         print(json.dumps(line), flush=True)
     slab.close()
 
