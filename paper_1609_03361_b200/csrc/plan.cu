@@ -175,7 +175,7 @@ struct sf_plan {
         int* cp = nullptr;
         float* cw = nullptr;
         size_t cap_tiles = 0, cap_cells = 0, cap_contrib = 0;
-    } fused;
+    } fused, fused_adj;  // fused_adj: FWI adjoint + gradient kernel (its own tiles)
     bool fused_disabled = false;  // SF_NO_FUSED_SPARSE=1
 
     ~sf_plan();
@@ -898,6 +898,23 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
             T.grad = p.tm_grad;
             T.gradp = grad;
             T.zchunk = p.zchunk_grad;
+            if (epi && epi->inj && p.fused_adj.ok && epi->inj->np > 0 && epi->inj->ncells > 0) {
+                T.inj_tile_start = p.fused_adj.tile_start;
+                T.inj_cell = p.fused_adj.cell;
+                T.inj_start = p.fused_adj.start;
+                T.inj_cp = p.fused_adj.cp;
+                T.inj_cw = p.fused_adj.cw;
+                T.inj_row = epi->inj->series + epi->inj_row * epi->inj->np;
+                T.mfield = p.m;
+                T.inj_scale = p.ac.src_scale;
+            }
+            if (epi && epi->smp && epi->smp->np > 0) {
+                T.smp_field = cur;
+                T.smp_ci = epi->smp->ci;
+                T.smp_w = epi->smp->w;
+                T.smp_out = epi->smp->series + epi->smp_row * epi->smp->np;
+                T.smp_np = static_cast<int>(epi->smp->np);
+            }
             launch_vec_grad(p.ac.radius, p.grid_grad, p.smem_grad, p.stream, T);
             return;
         }
@@ -1409,14 +1426,31 @@ void enqueue_fwi_adjoint(Plan& p) {
     const int64_t L = p.slot_elems;
     for (int s = 0; s < 3; ++s) SF_CUDA(cudaMemsetAsync(p.v[s], 0, sizeof(float) * L, p.stream));
     SF_CUDA(cudaMemsetAsync(p.grad, 0, sizeof(float) * L, p.stream));
+    // the gradient kernel (t < nt) carries the residual injection of its step
+    // and the source sampling of the step before in its epilogue when the
+    // tile-sorted CSR exists; the first step (no gradient term) does not
+    const bool fused = p.fused_adj.ok && !p.fused_disabled;
     for (int64_t t = p.nt; t >= 1; --t) {
         float* out = p.v[(t + 2) % 3];
         const float* cur = p.v[t % 3];
         const float* prev = p.v[(t + 1) % 3];
-        if (t <= p.nt - 1)  // term for time t+1: v(t+2) is still in `out`
+        if (t <= p.nt - 1) {  // term for time t+1: v(t+2) is still in `out`
+            if (fused) {
+                Epilogue epi;
+                epi.inj = &p.rec;
+                epi.inj_row = t - 1;
+                if (t <= p.nt - 2) {  // step t+1 sampled row t; step nt sampled itself
+                    epi.smp = &p.src;
+                    epi.smp_row = t;
+                }
+                launch_stencil(p, out, cur, prev, p.grad, p.hist + (t + 2) * L, nullptr, &epi);
+                if (t == 1) launch_sample(p, p.src, out, 0);
+                continue;
+            }
             launch_stencil(p, out, cur, prev, p.grad, p.hist + (t + 2) * L);
-        else
+        } else {
             launch_stencil(p, out, cur, prev);
+        }
         launch_inject_sample(p, p.rec, p.src, out, t - 1);
     }
     if (p.nt >= 1) {  // term for time 1
@@ -1462,24 +1496,19 @@ void enqueue_steps(Plan& p, int64_t b, int64_t e) {
 // contributions still in ascending point order. Rebuilt when the points or
 // the tile geometry change; not built (fused path off) when a cell lies
 // outside the planes / tiles the stencil kernel covers.
-void ensure_fused(Plan& p) {
-    // FWI: the forward sweep (p.ac is the forward set outside the adjoint)
-    if (p.fused_disabled || (p.kind != Plan::ACOUSTIC && p.kind != Plan::FWI) || p.ndim != 3 ||
-        !p.use_vec || p.use_vecq || p.slab || p.nccl_comm) {
-        p.fused.ok = false;
-        return;
-    }
-    const PointSet& inj = p.ac.forward ? p.src : p.rec;
-    const int64_t tx = 32 * p.tile_nx, ty = 4 * p.vec_warps * p.vec_rpl / p.tile_nx;
-    const uint64_t key[8] = {inj.version + 1, p.grid3.x, p.grid3.y, p.grid3.z,
-                             static_cast<uint64_t>(p.zchunk), static_cast<uint64_t>(tx),
+// Build (or keep) one tile-sorted CSR: `inj`'s cells grouped by the CTA of
+// the launch geometry (grid, zchunk, tx x ty tiles over planes [z0, z1)).
+void build_fused(Plan& p, sf_plan::FusedSparse& f, const PointSet& inj, dim3 grid, int zchunk,
+                 int64_t tx, int64_t ty) {
+    const uint64_t key[8] = {inj.version + 1, grid.x, grid.y, grid.z,
+                             static_cast<uint64_t>(zchunk), static_cast<uint64_t>(tx),
                              static_cast<uint64_t>(ty),
                              (static_cast<uint64_t>(p.z0) << 32) | static_cast<uint32_t>(p.z1)};
-    if (std::memcmp(key, p.fused.key, sizeof key) == 0) return;
-    std::memcpy(p.fused.key, key, sizeof key);
+    if (std::memcmp(key, f.key, sizeof key) == 0) return;
+    std::memcpy(f.key, key, sizeof key);
     clear_graphs(p);
-    p.fused.ok = false;
-    const int64_t gx = p.grid3.x, gy = p.grid3.y, gz = p.grid3.z;
+    f.ok = false;
+    const int64_t gx = grid.x, gy = grid.y, gz = grid.z;
     const int64_t ntiles = gx * gy * gz;
     const int nc = inj.ncells;
     std::vector<int64_t> tile(static_cast<size_t>(nc));
@@ -1487,7 +1516,7 @@ void ensure_fused(Plan& p) {
         const int64_t off = inj.h_cells[i];
         const int64_t a0 = off / p.plane, a1 = (off % p.plane) / p.pitch, a2 = off % p.pitch;
         if (a0 < p.z0 || a0 >= p.z1 || a2 >= gx * tx || a1 >= gy * ty) return;
-        tile[i] = a2 / tx + gx * (a1 / ty + gy * ((a0 - p.z0) / p.zchunk));
+        tile[i] = a2 / tx + gx * (a1 / ty + gy * ((a0 - p.z0) / zchunk));
         if (tile[i] >= ntiles) return;
     }
     std::vector<int> order(static_cast<size_t>(nc));
@@ -1498,6 +1527,13 @@ void ensure_fused(Plan& p) {
     std::vector<int> start, cp;
     std::vector<float> cw;
     for (int i = 0; i < nc; ++i) ++tstart[tile[i] + 1];
+    // dense point sets (e.g. a full receiver grid injecting residuals) would
+    // pile thousands of cells onto the few CTAs of one z-chunk, serialised in
+    // their epilogue: a grid-wide injection kernel is faster there (measured,
+    // C5 adjoint +5 %). Fuse only while every CTA has at most one cell per
+    // consumer thread.
+    for (int64_t t = 0; t < ntiles; ++t)
+        if (tstart[t + 1] > 128) return;
     for (int64_t t = 0; t < ntiles; ++t) tstart[t + 1] += tstart[t];
     for (int oi : order) {
         cell.push_back(inj.h_cells[oi]);
@@ -1513,7 +1549,6 @@ void ensure_fused(Plan& p) {
         cp.push_back(0);
         cw.push_back(0.0f);
     }
-    auto& f = p.fused;
     if (static_cast<size_t>(ntiles + 1) > f.cap_tiles) {
         dfree(f.tile_start);
         f.cap_tiles = static_cast<size_t>(ntiles + 1);
@@ -1542,11 +1577,31 @@ void ensure_fused(Plan& p) {
     f.ok = true;
 }
 
+// Tile-sorted copies of the injection CSR for the fused epilogue: cells of
+// CTA b (launch order) in [tile_start[b], tile_start[b+1]), each cell's
+// contributions still in ascending point order. Rebuilt when the points or
+// the tile geometry change; not built (fused path off) when a cell lies
+// outside the planes / tiles the stencil kernel covers.
+void ensure_fused(Plan& p) {
+    // FWI: the forward sweep (p.ac is the forward set outside the adjoint)
+    if (p.fused_disabled || (p.kind != Plan::ACOUSTIC && p.kind != Plan::FWI) || p.ndim != 3 ||
+        !p.use_vec || p.use_vecq || p.slab || p.nccl_comm) {
+        p.fused.ok = false;
+        p.fused_adj.ok = false;
+        return;
+    }
+    const PointSet& inj = p.ac.forward ? p.src : p.rec;
+    build_fused(p, p.fused, inj, p.grid3, p.zchunk, 32 * p.tile_nx,
+                4 * p.vec_warps * p.vec_rpl / p.tile_nx);
+    if (p.kind == Plan::FWI)  // adjoint + gradient kernel: 64 x 8 tiles, rec injects
+        build_fused(p, p.fused_adj, p.rec, p.grid_grad, p.zchunk_grad, 64, 8);
+}
+
 // Steps [b, e) as one cached CUDA graph (the OpenMP team + barriers of the
 // generated loop become graph edges; launches cost ~graph-node latency).
 void run_steps(Plan& p, int64_t b, int64_t e) {
     if (b >= e && b >= 0) return;
-    if (b >= 0 || b == kFwiForward) ensure_fused(p);
+    if (b >= 0 || b == kFwiForward || b == kFwiAdjoint) ensure_fused(p);
     auto key = std::make_pair(b, e);
     auto it = p.graphs.find(key);
     if (it == p.graphs.end()) {
@@ -1963,6 +2018,11 @@ sf_plan::~sf_plan() {
     sfb::dfree(fused.start);
     sfb::dfree(fused.cp);
     sfb::dfree(fused.cw);
+    sfb::dfree(fused_adj.tile_start);
+    sfb::dfree(fused_adj.cell);
+    sfb::dfree(fused_adj.start);
+    sfb::dfree(fused_adj.cp);
+    sfb::dfree(fused_adj.cw);
     sfb::dfree(hist);
     sfb::dfree(grad);
     for (float* s : v) sfb::dfree(s);
