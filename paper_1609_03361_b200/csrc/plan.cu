@@ -11,6 +11,8 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -614,16 +616,24 @@ void launch_vec(int r, int warps, int nx, int rpl, dim3 g, size_t smem, cudaStre
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
+    // resolved once (thread-safe static initialisation); a failed lookup is
+    // retried on the next call rather than cached
+    static const PFN_cuTensorMapEncodeTiled_v12000 cached = [] {
         void* ptr = nullptr;
         cudaDriverEntryPointQueryResult q;
-        SF_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
-        if (q != cudaDriverEntryPointSuccess || !ptr)
-            throw Status(SF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-    }
-    return fn;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            ptr = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }();
+    if (cached) return cached;
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SF_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !ptr)
+        throw Status(SF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
 }
 
 // 3D map over one padded field: dims (n2, n1, n0), row/plane strides in
@@ -1043,6 +1053,8 @@ constexpr int kNcclFloat32 = 7;  // ncclFloat32 in nccl.h
 const NcclApi& nccl() {
     static NcclApi api;
     static bool loaded = false;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
     if (loaded) return api;
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
@@ -1303,12 +1315,16 @@ template <int R>
 void launch_diffusion_tb_t(dim3 g, cudaStream_t st, const DiffusionTBArgs& A) {
     constexpr int TMAX = 8 / R > 0 ? 8 / R : 1;
     using L = TbLayout<R, kTbTile, TMAX>;
-    static bool attr = false;
-    if (!attr) {
+    // function attributes are per device: remember which devices have it
+    static std::atomic<uint64_t> done{0};
+    int dev = 0;
+    SF_CUDA(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(done.load() & bit)) {
         SF_CUDA(cudaFuncSetAttribute(&diffusion_tb_kernel<R, kTbTile, TMAX>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(L::smem)));
-        attr = true;
+        done.fetch_or(bit);
     }
     diffusion_tb_kernel<R, kTbTile, TMAX><<<g, 256, L::smem, st>>>(A);
 }
