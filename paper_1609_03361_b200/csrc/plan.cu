@@ -7,6 +7,19 @@
 //        for t: aliases (K6) -> stencil (K2/K3) -> inject (K4) -> sample (K5)
 // Here: plan create = build time (constants folded, buffers allocated in HBM),
 // apply = H2D, nt steps replayed from a cached CUDA graph, D2H.
+//
+// Layout of this file:
+//   plan state (sf_plan, PointSet)          host <-> HBM transfers, point CSR
+//   kernel tables + launchers               per-thread-load / scalar TMA /
+//                                           vector ring / queue-vector / 2D /
+//                                           diffusion; tensor maps; PDL
+//   launch_stencil / sparse launches        incl. the fused sparse epilogue
+//   NCCL (dlopen'd) halo exchange           slab steps, in-process chain
+//   step enqueue: acoustic, diffusion (temporal blocking), FWI forward/adjoint
+//   tile-sorted injection CSR, graphs       build_fused, ensure_fused, run_steps
+//   geometry                                chunk_grid, set_grid, enable_tma
+//   plan construction, upload / download    setup_acoustic, upload_any, ...
+//   autotune, SFG1 + text I/O, self-test    then the extern "C" entry points
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -2072,13 +2085,8 @@ struct StencilConfig {
     int tile_nx, tile_ty, vec_warps, stages;
 };
 
-void drop_graphs(Plan& p) {
-    for (auto& kv : p.graphs) cudaGraphExecDestroy(kv.second);
-    p.graphs.clear();
-}
-
 void apply_config(Plan& p, const StencilConfig& c) {
-    drop_graphs(p);
+    clear_graphs(p);
     p.use_tma = p.use_vec = p.use_vecq = false;
     p.tile_nx = c.tile_nx;
     p.tile_ty = c.tile_ty;
@@ -2186,7 +2194,7 @@ extern "C" int sf_plan_autotune(sf_plan* p, int64_t tune_steps, int repeats, sf_
                 best_ms = med;
                 best = c;
             }
-            drop_graphs(*p);
+            clear_graphs(*p);
         }
         apply_config(*p, best);
         restore(false);
