@@ -310,6 +310,8 @@ class Operator:
         for e in ents[: min(n.value, 64)]:
             desc = (f"{self.KINDS[e.kind]} nx={e.tile_nx} ty={e.tile_ty} warps={e.vec_warps} "
                     f"stages={e.stages}")
+            if e.kind == 2:  # vector ring: rows of four points per lane
+                desc += f" rows/lane={max(1, e.tile_ty * e.tile_nx // (4 * e.vec_warps))}"
             rep.append((desc, e.median_ms / 1e3))
         best = min(rep, key=lambda x: x[1]) if rep else None
         return rep, best

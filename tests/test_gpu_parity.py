@@ -520,3 +520,18 @@ def test_step_ranges_and_tile_edge_points(sf, port, order, shape, forward, split
         _lib.lib.sf_plan_destroy(plan)
     assert_parity(bufs[0], want_u)
     assert_parity(bufs[6] if forward else bufs[3], want_rec if forward else want_src)
+
+
+def test_bench_helpers(sf):
+    """bench_acoustic / bench_diffusion: the reference's restore-and-median
+    protocol; the sweep reports every kernel configuration and leaves the
+    operator producing the oracle's result."""
+    from paper_1609_03361_b200.benchmarks import bench_acoustic, bench_diffusion, format_bench
+    model = sf.AcousticModel(shape=(36, 40, 44), nt=6, boundary_width=4, space_order=4)
+    lines = bench_acoustic(model, runs=2)
+    assert lines[0].variant == "apply" and lines[0].median_s > 0
+    assert any(l.variant == "resident" and "vector-tma" in l.plan for l in lines)
+    assert all(l.median_s > 0 for l in lines)
+    d = bench_diffusion(sf.DiffusionConfig(nx=64, ny=64, nt=10), runs=2)
+    assert d[0].scenario == "diffusion" and d[0].median_s > 0
+    assert format_bench(lines + d).count("\n") == len(lines) + 1
