@@ -81,3 +81,35 @@ def test_slab_desc_validation():
     assert _lib.lib.sf_acoustic_plan_create_slab(C.byref(d), C.byref(ok), 0, C.byref(plan)) == 0
     _lib.lib.sf_plan_destroy(plan)
     del sf
+
+
+def test_nccl_single_rank_plumbing(port):
+    """The one-process-per-GPU transport on this box's single GPU: NCCL is
+    dlopen'd (PyTorch's copy when loaded), a 1-rank communicator is created
+    from sf_nccl_unique_id and attached to a whole-grid slab, and the run is
+    bitwise the single-domain plan (no neighbour, so no exchange is issued)."""
+    import torch  # noqa: F401  (brings PyTorch's NCCL into the process)
+    import paper_1609_03361_b200 as sf
+    from paper_1609_03361_b200.slab import SlabPartition, SlabRun, assemble, nccl_unique_id
+    from test_gpu_parity import run_plan_raw
+    shape, order, nt = (40, 36, 44), 8, 12
+    r = order // 2
+    rng = np.random.default_rng(3)
+    v = 1500.0 + 3000.0 * rng.random(shape)
+    m, eta = port.medium_from_velocity(v, 5, 10.0, 1500.0)
+    dt = min(0.4 * 10.0 / 4500.0, port.stable_dt(3, order, 10.0, 4500.0, 4500.0))
+    src_ci, src_w = port.interp(np.array([[200.0, 180.0, 210.0]]), 10.0, shape)
+    rec_ci, rec_w = port.interp(np.array([[150.0, 100.0 + 9 * i, 120.0] for i in range(7)]),
+                                10.0, shape)
+    src = rng.standard_normal((nt, 1)).astype(np.float32)
+    rec = np.zeros((nt, 7), np.float32)
+    ref = run_plan_raw(sf, shape, order, True, dt, 10.0, nt, m, eta, src.copy(), src_ci, src_w,
+                       rec.copy(), rec_ci, rec_w)
+    slab = SlabRun(SlabPartition.split(shape[0], r, 1, 0), shape, order, True, nt, dt, 10.0, m,
+                   eta, src, src_ci, src_w, rec, rec_ci, rec_w)
+    slab.attach_nccl(nccl_unique_id(), 1, 0)
+    slab.run(0, nt)
+    u, _, r_tr = assemble([slab], shape, nt, 1, 7)
+    assert np.array_equal(bits(u), bits(ref[0]))
+    assert np.array_equal(bits(r_tr), bits(ref[6]))
+    slab.close()
