@@ -644,7 +644,8 @@ def run_b200_slabs(args, world, rank, local):
     slab = SlabRun(part, gshape, model.space_order, True, model.nt, model.dt, model.spacing,
                    m.data, eta.data, ser, src_ci, src_w, rec, rec_ci, rec_w, device=local)
     obj = [nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
+    if world > 1:
+        dist.broadcast_object_list(obj, src=0)
     slab.attach_nccl(obj[0], world, rank)
     for _ in range(args.warmup):
         slab.run(0, model.nt)
@@ -666,7 +667,15 @@ def run_b200_slabs(args, world, rank, local):
     for e in gshape:
         pts *= e - 2 * r
     value = pts * model.nt / (ms_per_step / 1e3) / 1e9
-    # e2e: upload host slices, run, download, every step
+    # e2e: upload host slices, run, download, every step (pinned host buffers,
+    # as in the single-GPU arm)
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
+        arr = t.numpy()
+        arr[...] = a
+        return arr, t
+    keep = [pinned(b) for b in slab.bufs]
+    slab.bufs = [k[0] for k in keep]
     barrier(world)
     t_e = time.perf_counter()
     for _ in range(args.steps):
@@ -713,6 +722,9 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # exercise the multi-GPU slab path (NCCL communicator, slab plans) with a
+    # single rank: validates the N > 1 code on a one-GPU box
+    ap.add_argument("--force-slabs", action="store_true")
     args = ap.parse_args()
     world, rank, local = dist_init(args)
     try:
@@ -725,7 +737,7 @@ def main():
         elif kind == "fwi":
             if rank == 0:
                 run_b200_fwi(args, world, rank, local)
-        elif world > 1:
+        elif world > 1 or args.force_slabs:
             run_b200_slabs(args, world, rank, local)
         else:
             run_b200_arm(args, world, rank, local)
