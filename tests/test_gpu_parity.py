@@ -562,3 +562,49 @@ def test_full_size_config_bitwise(sf, port, cfg):
                       s.src.w.data, rec, s.rec.ci.data, s.rec.w.data, model.nt)
     assert np.array_equal(bits(s.field.data), bits(u))
     assert np.array_equal(bits(s.rec.data.data), bits(rec))
+
+
+@pytest.mark.parametrize("shape,order,ns,nr,nt", [
+    ((9, 9, 9), 8, 1, 1, 1),        # interior of a single point per axis
+    ((10, 40, 70), 8, 0, 3, 4),     # no sources
+    ((30, 20, 33), 4, 2, 0, 5),     # no receivers
+    ((18, 17, 130), 16, 1, 2, 3),   # order 16 on a thin grid
+    ((6, 7, 5), 2, 3, 3, 6),        # tiny grid, order 2
+])
+@pytest.mark.parametrize("forward", [True, False])
+def test_degenerate_shapes_and_empty_point_sets(sf, port, shape, order, ns, nr, nt, forward):
+    rng = np.random.default_rng(sum(shape) + order)
+    h = 10.0
+    r = order // 2
+    v = 1500.0 + 3000.0 * rng.random(shape)
+    m, eta = port.medium_from_velocity(v, 2, h, 1500.0)
+    dt = min(0.4 * h / 4500.0, port.stable_dt(3, order, h, 4500.0, 4500.0))
+
+    def pts(n):
+        if n == 0:
+            return np.zeros((0, 3), np.int32), np.zeros((0, 8), np.float32)
+        c = np.stack([rng.uniform(0.2 * h, (e - 1.2) * h, n) for e in shape], 1)
+        return port.interp(c, h, shape)
+    src_ci, src_w = pts(ns)
+    rec_ci, rec_w = pts(nr)
+    u0 = (1e-3 * rng.standard_normal((3,) + shape)).astype(np.float32)
+    src = (rng.standard_normal((nt, ns)) if forward else np.zeros((nt, ns))).astype(np.float32)
+    rec = (np.zeros((nt, nr)) if forward else rng.standard_normal((nt, nr))).astype(np.float32)
+    if ns == 0 or nr == 0:
+        # a zero-extent sparse series is rejected, as the reference's
+        # create_array rejects it (grid.cpp:179-188)
+        with pytest.raises(sf.InvalidShapeError):
+            run_plan_raw(sf, shape, order, forward, dt, h, nt, m, eta, src, src_ci, src_w, rec,
+                         rec_ci, rec_w, u=u0.copy())
+        return
+    out = run_plan_raw(sf, shape, order, forward, dt, h, nt, m, eta, src.copy(), src_ci, src_w,
+                       rec.copy(), rec_ci, rec_w, u=u0.copy())
+    coefs = port.coefs(3, order, forward, dt, h)
+    u = u0.copy()
+    if forward:
+        port.acoustic_run(coefs, u, m, eta, src, src_ci, src_w, rec, rec_ci, rec_w, nt)
+        assert_parity(out[6], rec)
+    else:
+        port.acoustic_run(coefs, u, m, eta, rec, rec_ci, rec_w, src, src_ci, src_w, nt)
+        assert_parity(out[3], src)
+    assert_parity(out[0], u)
