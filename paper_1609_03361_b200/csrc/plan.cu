@@ -914,6 +914,12 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
         for (int k = 0; k < 3; ++k) T.tc[k] = p.ac.tc[k];
         T.c0 = p.ac.c0;
         for (int j = 0; j < 8; ++j) T.cj[j] = p.ac.cj[j];
+        T.pk_one = f2_splat_host(1.0f);
+        T.pk_ce = f2_splat_host(T.ce);
+        T.pk_cm = f2_splat_host(T.cm);
+        for (int k = 0; k < 3; ++k) T.pk_tc[k] = f2_splat_host(T.tc[k]);
+        T.pk_c0 = f2_splat_host(T.c0);
+        for (int j = 0; j < 8; ++j) T.pk_cj[j] = f2_splat_host(T.cj[j]);
         if (grad) {
             T.old = *mo.pme;
             T.uh = *mu.pme;

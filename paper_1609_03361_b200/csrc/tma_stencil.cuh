@@ -26,6 +26,7 @@
 #include <cstdint>
 
 #include "kernels.cuh"
+#include "pk2.cuh"
 
 namespace sfb {
 
@@ -53,6 +54,9 @@ struct TmaStencilArgs {
     float tc[3];
     float c0;
     float cj[8];
+    // the same constants as (c, c) pairs for the packed fp32x2 kernels, and
+    // the opaque ONE their sums multiply by (pk2.cuh)
+    unsigned long long pk_one, pk_ce, pk_cm, pk_tc[3], pk_c0, pk_cj[8];
     // Fused sparse epilogue (vector ring kernel): after its last plane a CTA
     // (1) injects this step's sources into the cells of its own tile (a
     // tile-sorted copy of the injection CSR: cells [tile_start[b],
