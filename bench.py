@@ -374,7 +374,12 @@ def run_b200_arm(args, world, rank, local):
     value = world * pts * model.nt / (ms_per_step / 1e3) / 1e9
     # stencil-only pass: average launch duration of the dominant kernel
     stencil_launch_ms = sten_ms / model.nt
-    alg_bytes = 20 * pts
+    # compulsory bytes: read u(t), u(t-1), m, eta, write u(t+1) = 20 B/pt,
+    # less the eta boxes the kernel skips because they are all zero (the
+    # undamped interior) -- those bytes are not needed, so they are not
+    # counted as achieved bandwidth
+    eta_skip = op.eta_skip_fraction()
+    alg_bytes = (20 - 4 * eta_skip) * pts
     peak, peak_kind = load_peaks()
     achieved = alg_bytes / (stencil_launch_ms / 1e3) / 1e9
     traffic = None
@@ -414,7 +419,7 @@ def run_b200_arm(args, world, rank, local):
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_kind,
                      "kernel": f"3D stencil (radius {r}) avg launch {stencil_launch_ms * 1e3:.1f} us",
-                     "alg_bytes_per_launch": alg_bytes},
+                     "alg_bytes_per_launch": alg_bytes, "eta_boxes_skipped": eta_skip},
         # second lens for the high orders: the reference's exact fp32 operation
         # count (no FMA contraction: 17 + 13r mul/add with c_j*temp3 shared
         # across the 6 neighbours of one offset, + 4 for the correctly rounded
@@ -582,6 +587,10 @@ def run_b200_fwi(args, world, rank, local):
         pts *= e - 2 * r
     value = 2 * pts * nt / ((fwd + adj) / 1e3) / 1e9
     peak, peak_kind = load_peaks()
+    # the all-zero eta boxes both sweeps skip (the forward tiling's fraction,
+    # applied to both) are not counted as achieved bytes
+    skip = plan.eta_skip_fraction()
+    bf, ba = 20 - 4 * skip, 36 - 4 * skip
     line = {
         "metric": "GPts/s (grid-point updates/sec)", "value": value, "unit": "GPts/s",
         "n_gpus": 1, "steps": args.steps, "warmup": 1, "ms_per_step": fwd + adj,
@@ -592,11 +601,11 @@ def run_b200_fwi(args, world, rank, local):
                    "forward_ms": fwd, "adjoint_gradient_ms": adj,
                    "grad_abs_max": float(np.abs(grad).max())},
         "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_kind,
-                     "forward_achieved": 20 * pts * nt / (fwd / 1e3) / 1e9,
-                     "adjoint_achieved": 36 * pts * nt / (adj / 1e3) / 1e9,
-                     "achieved": (20 + 36) * pts * nt / ((fwd + adj) / 1e3) / 1e9,
-                     "frac": (20 + 36) * pts * nt / ((fwd + adj) / 1e3) / 1e9 / peak,
-                     "traffic": None},
+                     "forward_achieved": bf * pts * nt / (fwd / 1e3) / 1e9,
+                     "adjoint_achieved": ba * pts * nt / (adj / 1e3) / 1e9,
+                     "achieved": (bf + ba) * pts * nt / ((fwd + adj) / 1e3) / 1e9,
+                     "frac": (bf + ba) * pts * nt / ((fwd + adj) / 1e3) / 1e9 / peak,
+                     "traffic": None, "eta_boxes_skipped": skip},
         "e2e": {"value": 2 * pts * nt / e2e_s / 1e9, "unit": "GPts/s",
                 "h2d_bytes_per_step": m.data.nbytes * 2 + residual.nbytes + src.nbytes,
                 "d2h_bytes_per_step": grad.nbytes + rec_out.nbytes},
@@ -705,12 +714,17 @@ def run_b200_slabs(args, world, rank, local):
         }
         peak, peak_kind = load_peaks()
         own_pts = pts // world  # each rank updates its own slab's interior share
-        achieved = 20 * own_pts / (sten_ms / model.nt / 1e3) / 1e9
+        import ctypes
+        frac = ctypes.c_double()
+        sf.api.check(_lib.lib.sf_plan_eta_skip_fraction(slab.plan, ctypes.byref(frac)))
+        bpp = 20 - 4 * frac.value  # less the all-zero eta boxes the kernel skips
+        achieved = bpp * own_pts / (sten_ms / model.nt / 1e3) / 1e9
         line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                             "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
                             "kernel": f"3D stencil (radius {r}) per rank, avg launch "
                                       f"{sten_ms / model.nt * 1e3:.1f} us (stencil-only pass)",
-                            "alg_bytes_per_launch": 20 * own_pts}
+                            "alg_bytes_per_launch": bpp * own_pts,
+                            "eta_boxes_skipped": frac.value}
         print(json.dumps(line), flush=True)
     slab.close()
 

@@ -229,6 +229,12 @@ int sf_diffusion_constants(int order, int64_t alpha_num, int64_t alpha_den, int6
  * against __frcp_rn over all 2^32 float bit patterns; *mismatches = count. */
 int sf_selftest_reciprocal(int device, unsigned long long *mismatches);
 
+/* Measurement hook (no reference counterpart): fraction of the interior
+ * point updates per step whose eta box the vector kernels skip because it is
+ * all +0.0 (the undamped interior; the kernels then use 0.0f, bitwise the
+ * value they would have read). Valid after a run; 0 when the skip is off. */
+int sf_plan_eta_skip_fraction(sf_plan *plan, double *fraction);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,6 +40,7 @@ EXPORTS = [
     "sf_acoustic_plan_create_slab", "sf_slab_chain_run", "sf_nccl_unique_id",
     "sf_plan_attach_nccl", "sf_plan_autotune", "sf_plan_save_buffer", "sf_plan_load_buffer",
     "sf_plan_dump_csv", "sf_plan_save_series_text", "sf_selftest_reciprocal",
+    "sf_plan_eta_skip_fraction",
 ]
 
 
@@ -125,6 +126,7 @@ def _bind(lib):
     lib.sf_plan_dump_csv.argtypes = [_vp, C.c_char_p, C.c_char_p, C.c_long]
     lib.sf_plan_save_series_text.argtypes = [_vp, C.c_char_p, C.c_char_p]
     lib.sf_selftest_reciprocal.argtypes = [C.c_int, C.POINTER(C.c_ulonglong)]
+    lib.sf_plan_eta_skip_fraction.argtypes = [_vp, C.POINTER(C.c_double)]
     lib.sf_plan_autotune.argtypes = [_vp, C.c_int64, C.c_int, C.POINTER(TuneEntry), C.c_int,
                                      C.POINTER(C.c_int)]
     return lib

@@ -316,6 +316,13 @@ class Operator:
         best = min(rep, key=lambda x: x[1]) if rep else None
         return rep, best
 
+    def eta_skip_fraction(self):
+        """Fraction of interior point updates per step whose eta box the
+        vector kernels skip (all +0.0); measurement hook for the roofline."""
+        f = C.c_double()
+        check(lib.sf_plan_eta_skip_fraction(self._plan, C.byref(f)))
+        return f.value
+
     def time(self, stencil=True):
         """(total_ms, stencil_ms, kernel_launches) of one device-timed run."""
         tot = C.c_float()
@@ -673,6 +680,12 @@ class FwiPlan:
             lib.sf_plan_destroy(self._plan)
         except Exception:
             pass
+
+    def eta_skip_fraction(self):
+        """Forward sweep: fraction of point updates whose eta box is skipped."""
+        f = C.c_double()
+        check(lib.sf_plan_eta_skip_fraction(self._plan, C.byref(f)))
+        return f.value
 
     def gradient(self, m, eta, src, src_ci, src_w, rec_ci, rec_w, residual, want_v=False,
                  want_src=False):

@@ -192,6 +192,16 @@ struct sf_plan {
         size_t cap_tiles = 0, cap_cells = 0, cap_contrib = 0;
     } fused, fused_adj;  // fused_adj: FWI adjoint + gradient kernel (its own tiles)
     bool fused_disabled = false;  // SF_NO_FUSED_SPARSE=1
+    // all-zero eta boxes per (tile, plane) for the vector kernels
+    // (TmaStencilArgs::eta0); recomputed when eta is rewritten (eta_gen)
+    struct EtaFlags {
+        uint32_t* bits = nullptr;
+        size_t cap = 0;
+        int tx = 0, ty = 0, ntx = 0, nty = 0, words = 0;
+        uint64_t gen = 0;  // eta_gen the bits describe (0 = none)
+    } eta0, eta0_grad;
+    uint64_t eta_gen = 1;
+    bool eta_skip_disabled = false;  // SF_NO_ETA_SKIP=1
 
     ~sf_plan();
 };
@@ -703,10 +713,10 @@ void setup_tma(Plan& p) {
         int stages = 3;
         if (const char* env = std::getenv("SF_TMA_STAGES")) {
             const int v = std::atoi(env);
-            if (v >= 2 && v <= 16) stages = v;
+            if (v >= 2 && v <= 12) stages = v;
         }
-        if (p.stages_override >= 2) stages = p.stages_override;
-        p.tma_stages = stages;
+        if (p.stages_override >= 2) stages = std::min(p.stages_override, 12);
+        p.tma_stages = stages;  // <= 12: barriers + eta flags share 256 bytes
         p.tma_smem = vecq_smem_bytes(r, p.vec_warps, stages);
         for (int fwd = 0; fwd < 2; ++fwd) {
             const void* fn = fwd ? vecq_ptr<true>(r, p.vec_warps) : vecq_ptr<false>(r, p.vec_warps);
@@ -723,10 +733,10 @@ void setup_tma(Plan& p) {
             --stages;
         if (const char* env = std::getenv("SF_TMA_STAGES")) {
             const int v = std::atoi(env);
-            if (v >= 2 && v <= 16) stages = v;
+            if (v >= 2 && v <= 12) stages = v;
         }
-        if (p.stages_override >= 2) stages = p.stages_override;
-        p.tma_stages = stages;
+        if (p.stages_override >= 2) stages = std::min(p.stages_override, 12);
+        p.tma_stages = stages;  // <= 12: barriers + eta flags share 256 bytes
         p.tma_smem = vec_smem_bytes(r, p.vec_warps, stages, 3, nx, rpl);
         for (int fwd = 0; fwd < 2; ++fwd) {
             const void* fn = fwd ? vec_ptr<true>(r, p.vec_warps, nx, rpl)
@@ -914,6 +924,14 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
         for (int k = 0; k < 3; ++k) T.tc[k] = p.ac.tc[k];
         T.c0 = p.ac.c0;
         for (int j = 0; j < 8; ++j) T.cj[j] = p.ac.cj[j];
+        {
+            const sf_plan::EtaFlags& ef = grad ? p.eta0_grad : p.eta0;
+            if (ef.bits && ef.gen == p.eta_gen && (p.use_vec || p.use_vecq)) {
+                T.eta0 = ef.bits;
+                T.eta0_ntx = ef.ntx;
+                T.eta0_words = ef.words;
+            }
+        }
         T.pk_one = f2_splat_host(1.0f);
         T.pk_ce = f2_splat_host(T.ce);
         T.pk_cm = f2_splat_host(T.cm);
@@ -1632,11 +1650,51 @@ void ensure_fused(Plan& p) {
         build_fused(p, p.fused_adj, p.rec, p.grid_grad, p.zchunk_grad, 64, 8);
 }
 
+// eta0 bits for one tile shape (see TmaStencilArgs::eta0): recomputed on the
+// plan stream when eta was rewritten or the tile shape changed; a new buffer
+// drops the cached graphs (they hold the pointer).
+void compute_eta_flags(Plan& p, sf_plan::EtaFlags& f, int tx, int ty) {
+    if (f.gen == p.eta_gen && f.tx == tx && f.ty == ty) return;
+    const int n0 = static_cast<int>(p.n[0]), n1 = static_cast<int>(p.n[1]),
+              n2 = static_cast<int>(p.n[2]);
+    const int ntx = (n2 + tx - 1) / tx, nty = (n1 + ty - 1) / ty, words = (n0 + 31) / 32;
+    const size_t need = static_cast<size_t>(ntx) * nty * words;
+    if (need > f.cap) {
+        clear_graphs(p);
+        SF_CUDA(cudaStreamSynchronize(p.stream));
+        dfree(f.bits);
+        f.bits = dalloc<uint32_t>(need);
+        f.cap = need;
+    }
+    if (f.tx != tx || f.ty != ty) clear_graphs(p);
+    f.tx = tx;
+    f.ty = ty;
+    f.ntx = ntx;
+    f.nty = nty;
+    f.words = words;
+    eta_zero_flags_kernel<<<dim3(static_cast<unsigned>(ntx * nty), static_cast<unsigned>(words)), 256,
+                            0, p.stream>>>(p.eta, p.pitch, p.plane, n0, n1, n2, tx, ty, ntx, words,
+                                           f.bits);
+    SF_CUDA(cudaGetLastError());
+    f.gen = p.eta_gen;
+}
+
+void ensure_eta_flags(Plan& p) {
+    if (p.eta_skip_disabled || p.ndim != 3 || !p.eta || !(p.use_vec || p.use_vecq)) return;
+    if (p.kind != Plan::ACOUSTIC && p.kind != Plan::FWI) return;
+    if (p.use_vecq)
+        compute_eta_flags(p, p.eta0, 64, 2 * p.vec_warps);
+    else
+        compute_eta_flags(p, p.eta0, 32 * p.tile_nx, 4 * p.vec_warps * p.vec_rpl / p.tile_nx);
+    if (p.kind == Plan::FWI) compute_eta_flags(p, p.eta0_grad, 64, 8);
+}
+
 // Steps [b, e) as one cached CUDA graph (the OpenMP team + barriers of the
 // generated loop become graph edges; launches cost ~graph-node latency).
 void run_steps(Plan& p, int64_t b, int64_t e) {
     if (b >= e && b >= 0) return;
     if (b >= 0 || b == kFwiForward || b == kFwiAdjoint) ensure_fused(p);
+    ensure_eta_flags(p);
     auto key = std::make_pair(b, e);
     auto it = p.graphs.find(key);
     if (it == p.graphs.end()) {
@@ -1796,6 +1854,7 @@ void choose_geometry(Plan& p) {
 void enable_tma(Plan& p) {
     if (p.ndim != 3) return;
     if (const char* env = std::getenv("SF_NO_FUSED_SPARSE")) p.fused_disabled = env[0] == '1';
+    if (const char* env = std::getenv("SF_NO_ETA_SKIP")) p.eta_skip_disabled = env[0] == '1';
     if (const char* env = std::getenv("SF_NO_TMA"))
         if (env[0] == '1') return;
     const char* vec = std::getenv("SF_VEC");
@@ -1959,7 +2018,10 @@ void upload_acoustic(Plan& p, void* const* a) {
     for (int s = 0; s < 3; ++s)
         if (a[0]) h2d_field(p, p.slot[s], static_cast<const float*>(a[0]) + s * field_numel(p));
     if (a[1]) h2d_field(p, p.m, static_cast<const float*>(a[1]));
-    if (a[2]) h2d_field(p, p.eta, static_cast<const float*>(a[2]));
+    if (a[2]) {
+        h2d_field(p, p.eta, static_cast<const float*>(a[2]));
+        ++p.eta_gen;
+    }
     upload_points(p, p.src, static_cast<const float*>(a[3]), static_cast<const int*>(a[4]),
                   static_cast<const float*>(a[5]), fwd);
     upload_points(p, p.rec, static_cast<const float*>(a[6]), static_cast<const int*>(a[7]),
@@ -2058,6 +2120,8 @@ sf_plan::~sf_plan() {
     sfb::dfree(fused_adj.start);
     sfb::dfree(fused_adj.cp);
     sfb::dfree(fused_adj.cw);
+    sfb::dfree(eta0.bits);
+    sfb::dfree(eta0_grad.bits);
     sfb::dfree(hist);
     sfb::dfree(grad);
     for (float* s : v) sfb::dfree(s);
@@ -2400,6 +2464,34 @@ extern "C" int sf_plan_save_series_text(sf_plan* p, const char* name, const char
             std::fputc('\n', f);
         }
         if (std::fclose(f) != 0) throw Status(SF_ERR_INVALID, std::string("short write: ") + path);
+    });
+}
+
+extern "C" int sf_plan_eta_skip_fraction(sf_plan* p, double* fraction) {
+    return sfb::guard([&] {
+        if (!p || !fraction) throw sfb::Status(SF_ERR_INVALID, "null argument");
+        *fraction = 0.0;
+        const sf_plan::EtaFlags& f = p->eta0;
+        if (!f.bits || f.gen != p->eta_gen || p->ndim != 3) return;
+        std::vector<uint32_t> bits(static_cast<size_t>(f.ntx) * f.nty * f.words);
+        SF_CUDA(cudaStreamSynchronize(p->stream));
+        SF_CUDA(cudaMemcpy(bits.data(), f.bits, bits.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        const int64_t r = p->ac.radius;
+        auto overlap = [&](int64_t b, int64_t e, int64_t n) {
+            return std::max<int64_t>(0, std::min(e, n - r) - std::max(b, r));
+        };
+        double skipped = 0.0, total = 0.0;
+        for (int ty = 0; ty < f.nty; ++ty)
+            for (int tx = 0; tx < f.ntx; ++tx) {
+                const double pts = static_cast<double>(overlap(int64_t(tx) * f.tx, int64_t(tx + 1) * f.tx, p->n[2])) *
+                                   static_cast<double>(overlap(int64_t(ty) * f.ty, int64_t(ty + 1) * f.ty, p->n[1]));
+                for (int z = p->z0; z < p->z1; ++z) {
+                    total += pts;
+                    const uint32_t w = bits[(static_cast<size_t>(ty) * f.ntx + tx) * f.words + z / 32];
+                    if ((w >> (z % 32)) & 1u) skipped += pts;
+                }
+            }
+        *fraction = total > 0 ? skipped / total : 0.0;
     });
 }
 
@@ -2755,6 +2847,7 @@ int sf_fwi_gradient(sf_plan* p, const float* m, const float* eta, const float* s
         SF_CUDA(cudaSetDevice(p->device));
         sfb::h2d_field(*p, p->m, m);
         sfb::h2d_field(*p, p->eta, eta);
+        ++p->eta_gen;
         // forward: src injects, rec samples
         sfb::upload_points(*p, p->src, src, src_ci, src_w, true);
         sfb::upload_points(*p, p->rec, nullptr, rec_ci, rec_w, true);

@@ -57,6 +57,12 @@ struct TmaStencilArgs {
     // the same constants as (c, c) pairs for the packed fp32x2 kernels, and
     // the opaque ONE their sums multiply by (pk2.cuh)
     unsigned long long pk_one, pk_ce, pk_cm, pk_tc[3], pk_c0, pk_cj[8];
+    // eta boxes known to be all +0.0 (the undamped interior): bit z of
+    // eta0[(tile_y * eta0_ntx + tile_x) * eta0_words + z / 32]. The vector
+    // kernels skip those boxes' TMA loads and use 0.0f, which is bitwise the
+    // value they would have read (null = load every box).
+    const uint32_t* eta0;
+    int eta0_ntx, eta0_words;
     // Fused sparse epilogue (vector ring kernel): after its last plane a CTA
     // (1) injects this step's sources into the cells of its own tile (a
     // tile-sorted copy of the injection CSR: cells [tile_start[b],

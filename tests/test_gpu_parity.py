@@ -608,3 +608,54 @@ def test_degenerate_shapes_and_empty_point_sets(sf, port, shape, order, ns, nr, 
         port.acoustic_run(coefs, u, m, eta, rec, rec_ci, rec_w, src, src_ci, src_w, nt)
         assert_parity(out[3], src)
     assert_parity(out[0], u)
+
+
+@pytest.mark.parametrize("order", [4, 8, 12])
+def test_eta_zero_boxes_skipped_bitwise(sf, port, order):
+    """The vector kernels skip the TMA load of eta boxes that are all +0.0
+    and use 0.0f instead. Boxes holding -0.0, a single nonzero value, or
+    whose content changes between two applies of one plan (the flags are
+    recomputed when eta is re-uploaded) must still be read."""
+    import ctypes as C
+    from paper_1609_03361_b200 import _lib
+    shape = (44, 53, 100)
+    nt = 9
+    c = random_case(port, shape, order, seed=100 + order)
+    rng = c["rng"]
+    eta1 = np.zeros(shape, np.float32)
+    eta1[:6] = c["eta"][:6]             # damped top planes only
+    eta1[20, 30, 70] = 3.0e-4            # one nonzero value inside a box
+    eta1[25, 10:14, 40:44] = -0.0        # negative zeros: not skippable
+    eta2 = c["eta"].copy()               # second apply: the full sponge
+    eta2[30, 20, 50] = -0.0
+    d = _lib.AcousticDesc()
+    d.ndim = 3
+    for i, e in enumerate(shape):
+        d.shape[i] = e
+    d.space_order, d.forward, d.nt, d.dt, d.spacing = order, 1, nt, c["dt"], 10.0
+    d.n_src, d.n_rec = c["src_ci"].shape[0], c["rec_ci"].shape[0]
+    plan = C.c_void_p()
+    sf.api.check(_lib.lib.sf_acoustic_plan_create(C.byref(d), 0, C.byref(plan)))
+    coefs = port.coefs(3, order, True, c["dt"], 10.0)
+    try:
+        fractions = []
+        for eta in (eta1, eta2):
+            src = rng.standard_normal((nt, 3)).astype(np.float32)
+            u0 = (1e-3 * rng.standard_normal((3,) + shape)).astype(np.float32)
+            bufs = [u0.copy(), c["m"], eta, src.copy(), c["src_ci"], c["src_w"],
+                    np.zeros((nt, 17), np.float32), c["rec_ci"], c["rec_w"]]
+            bufs = [np.ascontiguousarray(b) for b in bufs]
+            sf.api.check(_lib.lib.sf_acoustic_apply(plan, *[b.ctypes.data for b in bufs]))
+            frac = C.c_double()
+            sf.api.check(_lib.lib.sf_plan_eta_skip_fraction(plan, C.byref(frac)))
+            fractions.append(frac.value)
+            u = u0.copy()
+            rec = np.zeros((nt, 17), np.float32)
+            port.acoustic_run(coefs, u, c["m"], eta, src, c["src_ci"], c["src_w"], rec,
+                              c["rec_ci"], c["rec_w"], nt)
+            assert_parity(bufs[0], u)
+            assert_parity(bufs[6], rec)
+        assert fractions[0] > 0.5          # most boxes of eta1 are +0.0
+        assert fractions[1] < fractions[0]  # the sponge leaves fewer
+    finally:
+        _lib.lib.sf_plan_destroy(plan)
