@@ -144,6 +144,7 @@ struct sf_plan {
     bool use_tma = false;
     bool use_vec = false;  // 4 points/thread, LDS.128 variant of the TMA pipeline
     bool use_vecq = false; // ... with the a0 neighbours in a register queue (radius >= 5)
+    bool vecq_ring = false;  // ... future a0 planes from a shared-memory core ring (vecq2)
     int vec_warps = 8;
     int vec_rpl = 1;  // vector kernel: rows of four points per lane (1 or 2)
     int tma_stages = 4;
@@ -529,9 +530,10 @@ size_t vec_smem_bytes(int r, int warps, int stages, int npme = 3, int nx = 2, in
 }
 
 template <bool FWD>
-const void* vecq_ptr(int r, int warps) {
+const void* vecq_ptr(int r, int warps, bool ring = false) {
 #define SF_V(RR)                                                                               \
     case RR:                                                                                   \
+        if (ring && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq2_kernel<RR, FWD, 4>); \
         return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 4>) \
                           : reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 8>);
     switch (r) {
@@ -541,19 +543,24 @@ const void* vecq_ptr(int r, int warps) {
 #undef SF_V
 }
 
-size_t vecq_smem_bytes(int r, int warps, int stages) {
+size_t vecq_smem_bytes(int r, int warps, int stages, bool ring = false) {
     const int ra = (r + 3) / 4 * 4;
     const int cur = ((64 + 2 * ra) * (2 * warps + 2 * r) * 4 + 127) / 128 * 128;
     const int pme = (64 * 2 * warps * 4 + 127) / 128 * 128;
+    if (ring)  // + the core box of plane z+R per stage and the ring of R + S core planes
+        return 256 + static_cast<size_t>(stages) * (cur + 4 * pme) + static_cast<size_t>(r + stages) * pme;
     return 256 + static_cast<size_t>(stages) * (cur + 3 * pme);
 }
 
 template <bool FWD>
-void launch_vecq(int r, int warps, dim3 g, size_t smem, cudaStream_t st, const TmaStencilArgs& A) {
+void launch_vecq(int r, int warps, dim3 g, size_t smem, cudaStream_t st, const TmaStencilArgs& A,
+                 bool ring = false) {
     const dim3 b(32 * warps);
 #define SF_V(RR)                                                                   \
     case RR:                                                                       \
-        if (warps == 4)                                                            \
+        if (ring && warps == 4)                                                    \
+            acoustic3d_vecq2_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);            \
+        else if (warps == 4)                                                       \
             acoustic3d_vecq_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);             \
         else                                                                       \
             acoustic3d_vecq_kernel<RR, FWD, 8><<<g, b, smem, st>>>(A);             \
@@ -710,16 +717,18 @@ void setup_tma(Plan& p) {
         }
     }
     if (p.use_vecq) {
-        int stages = 3;
+        const bool ring = p.vecq_ring && p.vec_warps == 4;
+        int stages = ring ? 2 : 3;  // ring: 2 stages keep 4 CTAs per SM within shared memory
         if (const char* env = std::getenv("SF_TMA_STAGES")) {
             const int v = std::atoi(env);
             if (v >= 2 && v <= 12) stages = v;
         }
         if (p.stages_override >= 2) stages = std::min(p.stages_override, 12);
         p.tma_stages = stages;  // <= 12: barriers + eta flags share 256 bytes
-        p.tma_smem = vecq_smem_bytes(r, p.vec_warps, stages);
+        p.tma_smem = vecq_smem_bytes(r, p.vec_warps, stages, ring);
         for (int fwd = 0; fwd < 2; ++fwd) {
-            const void* fn = fwd ? vecq_ptr<true>(r, p.vec_warps) : vecq_ptr<false>(r, p.vec_warps);
+            const void* fn = fwd ? vecq_ptr<true>(r, p.vec_warps, ring)
+                                 : vecq_ptr<false>(r, p.vec_warps, ring);
             if (!fn) throw Status(SF_ERR_INVALID, "queue vector stencil not compiled");
             SF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(p.tma_smem)));
@@ -966,10 +975,11 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
             return;
         }
         if (p.use_vecq) {
+            T.cur_core = *mc.pme;
             if (p.ac.forward)
-                launch_vecq<true>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T);
+                launch_vecq<true>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T, p.vecq_ring);
             else
-                launch_vecq<false>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T);
+                launch_vecq<false>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T, p.vecq_ring);
             return;
         }
         if (p.use_vec) {
@@ -1765,7 +1775,8 @@ void set_grid(Plan& p) {
                                    : p.tile_ty;
     int per_sm = 0;
     if (p.use_vecq) {
-        const void* fn = p.ac.forward ? vecq_ptr<true>(r, p.vec_warps) : vecq_ptr<false>(r, p.vec_warps);
+        const void* fn = p.ac.forward ? vecq_ptr<true>(r, p.vec_warps, p.vecq_ring)
+                                      : vecq_ptr<false>(r, p.vec_warps, p.vecq_ring);
         if (fn)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.vec_warps, p.tma_smem);
     } else if (p.use_vec) {
@@ -1855,6 +1866,13 @@ void enable_tma(Plan& p) {
     if (p.ndim != 3) return;
     if (const char* env = std::getenv("SF_NO_FUSED_SPARSE")) p.fused_disabled = env[0] == '1';
     if (const char* env = std::getenv("SF_NO_ETA_SKIP")) p.eta_skip_disabled = env[0] == '1';
+    {  // queue-vector stencil with the shared-memory core ring (vecq2), opt-in with
+       // SF_VECQ2=1: 122 instead of 160 registers at radius 8 (4 CTAs per SM), but
+       // the extra LDS.128 of the future planes make the LSU a second bottleneck:
+       // sustained order 12 747 vs 692 us, order 16 798 vs 768 us per step
+        const char* e = std::getenv("SF_VECQ2");
+        p.vecq_ring = e && e[0] == '1';
+    }
     if (const char* env = std::getenv("SF_NO_TMA"))
         if (env[0] == '1') return;
     const char* vec = std::getenv("SF_VEC");

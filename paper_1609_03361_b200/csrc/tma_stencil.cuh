@@ -40,6 +40,7 @@ struct TmaStencilArgs {
     CUtensorMap old;   // GRAD: the output slot before it is overwritten (v(t+2))
     CUtensorMap uh;    // GRAD: forward history, level lv_uh = u(t+1)
     CUtensorMap grad;  // GRAD: gradient accumulator
+    CUtensorMap cur_core;  // vecq2: un-halo'd box (TX, TY) of the cur level
     float* out;
     float* gradp;
     const float* cur_ptr;  // base of the cur map's field (vecq queue-head loads)

@@ -314,10 +314,11 @@ VARIANTS = [{}, {"SF_VEC": "0"}, {"SF_NO_TMA": "1"}, {"SF_VEC": "0", "SF_TMA": "
             {"SF_VEC": "0", "SF_NO_TMA": "1", "SF_TILE": "2,16"}, {"SF_VEC_NX": "1"},
             {"SF_VEC_NX": "1", "SF_TMA_STAGES": "4"}, {"SF_NO_FUSED_SPARSE": "1"},
             {"SF_VEC_RPL": "2"}, {"SF_VEC_RPL": "2", "SF_VEC_NX": "1"},
-            {"SF_VEC_RPL": "2", "SF_VEC_NX": "2", "SF_VEC_WARPS": "8"}]
+            {"SF_VEC_RPL": "2", "SF_VEC_NX": "2", "SF_VEC_WARPS": "8"}, {"SF_VECQ2": "1"},
+            {"SF_VECQ2": "1", "SF_TMA_STAGES": "3"}]
 
 
-@pytest.mark.parametrize("order", [2, 6, 8, 12])
+@pytest.mark.parametrize("order", [2, 6, 8, 12, 16])
 @pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 def test_every_kernel_variant_bitwise(sf, port, monkeypatch, order, env):
     """Each stencil kernel family (per-thread loads, scalar TMA, vector TMA
