@@ -100,7 +100,9 @@ __global__ void __launch_bounds__(256) diffusion_tb_kernel(const __grid_constant
     }
     mbar_wait(bar, 0);
     // (Packed fp32x2 arithmetic as in the acoustic kernels measured 3 %
-    // slower here in the sustained C1 run, 747 vs 769 GPts/s: scalar.)
+    // slower here in the sustained C1 run, 747 vs 769 GPts/s: scalar. The
+    // 64-wide core tile is the measured best for radius 1: 48 / 56 / 72 / 80
+    // / 96 (SF_TB_TILE) ran at 699 / 714 / 677 / 654 / 599 vs 759 GPts/s.)
     // Each thread updates 4 consecutive a1 cells per visit: one aligned
     // (4 + 2RA)-float window (LDS.128s) gives every a1 neighbour, one
     // LDS.128 per a0 row offset gives the a0 neighbours of all four.

@@ -126,6 +126,7 @@ struct sf_plan {
     float* staging = nullptr;  // dense copy of one field for host transfers
     float* dscratch[2] = {nullptr, nullptr};  // diffusion: second buffer pair (temporal blocking)
     bool diffusion_tb = true;
+    int tb_tile = 64;  // temporal-blocking core tile (radius 1 only: 64 / 72 / 80 / 96)
     CUtensorMap tm_dx[2], tm_dy[2];  // diffusion: 2D maps over slots / scratch (box SW x SW)
     float* m = nullptr;
     float* eta = nullptr;
@@ -1358,27 +1359,27 @@ void enqueue_diffusion_step(Plan& p, int64_t t) {
 // launch on 64x64 tiles, (64 + 16)^2-float ping-pong buffers.
 constexpr int kTbTile = 64;
 
-template <int R>
+template <int R, int TILE>
 void launch_diffusion_tb_t(dim3 g, cudaStream_t st, const DiffusionTBArgs& A) {
     constexpr int TMAX = 8 / R > 0 ? 8 / R : 1;
-    using L = TbLayout<R, kTbTile, TMAX>;
+    using L = TbLayout<R, TILE, TMAX>;
     // function attributes are per device: remember which devices have it
     static std::atomic<uint64_t> done{0};
     int dev = 0;
     SF_CUDA(cudaGetDevice(&dev));
     const uint64_t bit = 1ull << (dev & 63);
     if (!(done.load() & bit)) {
-        SF_CUDA(cudaFuncSetAttribute(&diffusion_tb_kernel<R, kTbTile, TMAX>,
+        SF_CUDA(cudaFuncSetAttribute(&diffusion_tb_kernel<R, TILE, TMAX>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(L::smem)));
         done.fetch_or(bit);
     }
-    diffusion_tb_kernel<R, kTbTile, TMAX><<<g, 256, L::smem, st>>>(A);
+    diffusion_tb_kernel<R, TILE, TMAX><<<g, 256, L::smem, st>>>(A);
 }
 
-int diffusion_box(int r) {
+int diffusion_box(int r, int tile = kTbTile) {
     const int tmax = 8 / r > 0 ? 8 / r : 1;
-    return kTbTile + 2 * ((tmax * r + 3) / 4 * 4);
+    return tile + 2 * ((tmax * r + 3) / 4 * 4);
 }
 
 void make_map_2d(CUtensorMap* map, const Plan& p, const float* base, uint32_t box) {
@@ -1397,16 +1398,25 @@ void make_map_2d(CUtensorMap* map, const Plan& p, const float* base, uint32_t bo
 
 int diffusion_tmax(int r) { return 8 / r > 0 ? 8 / r : 1; }
 
-void launch_diffusion_tb(int r, dim3 g, cudaStream_t st, const DiffusionTBArgs& A) {
+void launch_diffusion_tb(int r, int tile, dim3 g, cudaStream_t st, const DiffusionTBArgs& A) {
+    if (r == 1) {
+        switch (tile) {
+            case 48: return launch_diffusion_tb_t<1, 48>(g, st, A);
+            case 56: return launch_diffusion_tb_t<1, 56>(g, st, A);
+            case 72: return launch_diffusion_tb_t<1, 72>(g, st, A);
+            case 80: return launch_diffusion_tb_t<1, 80>(g, st, A);
+            case 96: return launch_diffusion_tb_t<1, 96>(g, st, A);
+            default: return launch_diffusion_tb_t<1, kTbTile>(g, st, A);
+        }
+    }
     switch (r) {
-        case 1: return launch_diffusion_tb_t<1>(g, st, A);
-        case 2: return launch_diffusion_tb_t<2>(g, st, A);
-        case 3: return launch_diffusion_tb_t<3>(g, st, A);
-        case 4: return launch_diffusion_tb_t<4>(g, st, A);
-        case 5: return launch_diffusion_tb_t<5>(g, st, A);
-        case 6: return launch_diffusion_tb_t<6>(g, st, A);
-        case 7: return launch_diffusion_tb_t<7>(g, st, A);
-        case 8: return launch_diffusion_tb_t<8>(g, st, A);
+        case 2: return launch_diffusion_tb_t<2, kTbTile>(g, st, A);
+        case 3: return launch_diffusion_tb_t<3, kTbTile>(g, st, A);
+        case 4: return launch_diffusion_tb_t<4, kTbTile>(g, st, A);
+        case 5: return launch_diffusion_tb_t<5, kTbTile>(g, st, A);
+        case 6: return launch_diffusion_tb_t<6, kTbTile>(g, st, A);
+        case 7: return launch_diffusion_tb_t<7, kTbTile>(g, st, A);
+        case 8: return launch_diffusion_tb_t<8, kTbTile>(g, st, A);
         default: throw Status(SF_ERR_INVALID, "radius out of range");
     }
 }
@@ -1421,8 +1431,8 @@ void enqueue_diffusion_tb(Plan& p, int64_t b, int64_t e) {
     float* X[2] = {p.slot[0], p.slot[1]};
     float* Y[2] = {p.dscratch[0], p.dscratch[1]};
     const int tmax = diffusion_tmax(p.dc.radius);
-    dim3 g(static_cast<unsigned>((p.n[1] + kTbTile - 1) / kTbTile),
-           static_cast<unsigned>((p.n[0] + kTbTile - 1) / kTbTile));
+    dim3 g(static_cast<unsigned>((p.n[1] + p.tb_tile - 1) / p.tb_tile),
+           static_cast<unsigned>((p.n[0] + p.tb_tile - 1) / p.tb_tile));
     bool in_x = true;
     for (int64_t t = b; t < e;) {
         const int T = static_cast<int>(std::min<int64_t>(tmax, e - t));
@@ -1441,7 +1451,7 @@ void enqueue_diffusion_tb(Plan& p, int64_t b, int64_t e) {
         A.c0 = p.dc.c0;
         A.has_c0 = p.dc.has_c0;
         for (int j = 0; j < 8; ++j) A.cj[j] = p.dc.cj[j];
-        launch_diffusion_tb(p.dc.radius, g, p.stream, A);
+        launch_diffusion_tb(p.dc.radius, p.tb_tile, g, p.stream, A);
         in_x = !in_x;
         t += T;
     }
@@ -2577,7 +2587,12 @@ int sf_diffusion_plan_create(const sf_diffusion_desc* d, int device, sf_plan** o
         for (int s = 0; s < 2; ++s) p->dscratch[s] = sfb::alloc_field(*p);
         if (const char* env = std::getenv("SF_DIFFUSION_TB")) p->diffusion_tb = env[0] != '0';
         if (p->diffusion_tb) {
-            const uint32_t box = static_cast<uint32_t>(sfb::diffusion_box(p->dc.radius));
+            if (const char* env = std::getenv("SF_TB_TILE")) {
+                const int t = std::atoi(env);
+                if (p->dc.radius == 1 && (t == 48 || t == 56 || t == 64 || t == 72 || t == 80 || t == 96))
+                    p->tb_tile = t;
+            }
+            const uint32_t box = static_cast<uint32_t>(sfb::diffusion_box(p->dc.radius, p->tb_tile));
             for (int s = 0; s < 2; ++s) {
                 sfb::make_map_2d(&p->tm_dx[s], *p, p->slot[s], box);
                 sfb::make_map_2d(&p->tm_dy[s], *p, p->dscratch[s], box);

@@ -309,6 +309,25 @@ def test_diffusion_temporal_blocking_vs_oracle(sf, port, order, n, nt):
     assert_parity(b.u.data, ref)
 
 
+@pytest.mark.parametrize("tile", ["48", "56", "72", "80", "96"])
+def test_diffusion_tile_variants_vs_oracle(sf, port, monkeypatch, tile):
+    """Radius-1 temporal blocking with every selectable core tile
+    (SF_TB_TILE; 64 is the measured default) on a ragged grid."""
+    from fractions import Fraction
+    monkeypatch.setenv("SF_TB_TILE", tile)
+    n, nt = 301, 21
+    rng = np.random.default_rng(int(tile))
+    u = rng.random((2, n, n)).astype(np.float32)
+    cfg = sf.DiffusionConfig(nx=n, ny=n, alpha=Fraction(1, 3), dx=Fraction(1, n - 1),
+                             dy=Fraction(1, n - 1), nt=nt, order=2)
+    b = sf.make_diffusion_operator(cfg)
+    b.u.data[...] = u
+    b.op.apply()
+    ref = u.copy()
+    port.diffusion_run(ref, 2, (1, 3), (1, n - 1), nt)
+    assert_parity(b.u.data, ref)
+
+
 VARIANTS = [{}, {"SF_VEC": "0"}, {"SF_NO_TMA": "1"}, {"SF_VEC": "0", "SF_TMA": "1"},
             {"SF_VECQ": "0"}, {"SF_VEC_WARPS": "8"}, {"SF_TMA_STAGES": "2"},
             {"SF_VEC": "0", "SF_NO_TMA": "1", "SF_TILE": "2,16"}, {"SF_VEC_NX": "1"},

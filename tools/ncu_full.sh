@@ -6,7 +6,7 @@ set -u
 mkdir -p gpurun_out/prof
 for item in $1; do
   name=${item%%:*}; cfg=${item##*:}
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:acoustic3d -s 10 -c 1 \
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:${KREGEX:-acoustic3d} -s 10 -c 1 \
     -f -o gpurun_out/prof/$name python bench.py --config $cfg --steps 1 --warmup 1 --no-cpu-baseline \
     > gpurun_out/prof/$name.log 2>&1
   ncu -i gpurun_out/prof/$name.ncu-rep --page raw --csv > gpurun_out/prof/$name.raw.csv 2>/dev/null
