@@ -298,11 +298,14 @@ def run_reference_arm(args, world, rank):
     if CONFIGS[args.config].get("kind") == "diffusion":
         c = CONFIGS[args.config]
         base = cpu_diffusion_sample(c["n"], c["nt"], args.cpu_budget)
+        pts = (c["n"] - 2) ** 2
         print(json.dumps({"impl": "reference", "metric": "GPts/s (grid-point updates/sec)",
                           "value": base["value"], "unit": "GPts/s", "n_gpus": world,
-                          "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+                          "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": pts * c["nt"] / (base["value"] * 1e9) * 1e3,
+                          "higher_is_better": True,
                           "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-                          "data": "synthetic", "config": {"workload": args.config},
+                          "data": "synthetic", "config": diffusion_config_block(c),
                           "cpu_baseline": base,
                           "e2e": {"value": base["value"], "unit": "GPts/s",
                                   "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
@@ -328,6 +331,14 @@ def run_reference_arm(args, world, rank):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def diffusion_config_block(c):
+    n, nt = c["n"], c["nt"]
+    return {"workload": f"c1: 2D diffusion {n}^2, order 2, {nt} steps, alpha 1/2, "
+                        f"dx 1/{n - 1}, dt = dx^2/4", "interior_points": (n - 2) ** 2,
+            "l2": "2 x 16 MiB slots are L2-resident (126 MB L2); HBM roofline is "
+                  "a lower bound here"}
 
 
 def config_block(args, model):
@@ -496,10 +507,7 @@ def run_b200_diffusion(args, world, rank, local):
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"c1: 2D diffusion {n}^2, order 2, {nt} steps, alpha 1/2, "
-                               f"dx 1/{n - 1}, dt = dx^2/4", "interior_points": pts,
-                   "l2": "2 x 16 MiB slots are L2-resident (126 MB L2); HBM roofline is "
-                         "a lower bound here"},
+        "config": diffusion_config_block(c),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
                      "kernel": f"diffusion_tb_kernel (temporal blocking, T=8 steps per "

@@ -185,3 +185,24 @@ def test_format_bench_matches_reference_text():
     assert txt == ("bench scenario=acoustic variant=apply plan=default runs=3 median_s=0.012346\n"
                    "bench scenario=acoustic variant=apply plan=SkippedTooLarge runs=0 "
                    "median_s=0.000000\n")
+
+
+def test_reference_arm_line_on_cpu():
+    """bench.py --impl reference (the driver's reference arm) runs the
+    reference's own CPU path and prints the contract's JSON line; C1 is the
+    reference's CPU-runnable case and takes a second here."""
+    import json
+    import subprocess
+    import sys
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libsf_ref.so")):
+        pytest.skip("reference not built (oracle/_ref)")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--config", "c1", "--steps", "1", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=600, check=True).stdout
+    line = json.loads(out.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "GPts/s" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"] == {"value": line["value"], "unit": "GPts/s", "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
+    assert line["config"]["workload"].startswith("c1: 2D diffusion 2048^2")
+    assert line["ms_per_step"] > 0 and line["higher_is_better"] is True
