@@ -64,6 +64,62 @@ __device__ __forceinline__ float diffusion_point(const DiffusionTBArgs& A, const
     return acc;
 }
 
+// Four consecutive a1 cells of one row in the emitted order (centre if its
+// weight is nonzero, a1 neighbours -R..-1, +1..+R, a0 neighbours -R..-1,
+// +1..+R), from the row's aligned window and the a0 neighbour row vectors
+// (up[j-1] = row -j, dn[j-1] = row +j).
+template <int R, int RA>
+__device__ __forceinline__ void diffusion_row4(const DiffusionTBArgs& A, const float* win,
+                                               const float4* up, const float4* dn, float* acc) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float t = __fmul_rn(A.cj[R - 1], win[RA + k - R]);
+        acc[k] = A.has_c0 ? __fadd_rn(__fmul_rn(A.c0, win[RA + k]), t) : t;
+    }
+#pragma unroll
+    for (int j = R - 1; j >= 1; --j)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] = __fadd_rn(acc[k], __fmul_rn(A.cj[j - 1], win[RA + k - j]));
+#pragma unroll
+    for (int j = 1; j <= R; ++j)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] = __fadd_rn(acc[k], __fmul_rn(A.cj[j - 1], win[RA + k + j]));
+#pragma unroll
+    for (int j = R; j >= 1; --j) {
+        const float vv[4] = {up[j - 1].x, up[j - 1].y, up[j - 1].z, up[j - 1].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] = __fadd_rn(acc[k], __fmul_rn(A.cj[j - 1], vv[k]));
+    }
+#pragma unroll
+    for (int j = 1; j <= R; ++j) {
+        const float vv[4] = {dn[j - 1].x, dn[j - 1].y, dn[j - 1].z, dn[j - 1].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] = __fadd_rn(acc[k], __fmul_rn(A.cj[j - 1], vv[k]));
+    }
+}
+
+template <int RA>
+__device__ __forceinline__ void load_window(const float* c, float* win) {
+#pragma unroll
+    for (int q = 0; q < (4 + 2 * RA) / 4; ++q) {
+        const float4 w = *reinterpret_cast<const float4*>(c - RA + 4 * q);
+        win[4 * q] = w.x;
+        win[4 * q + 1] = w.y;
+        win[4 * q + 2] = w.z;
+        win[4 * q + 3] = w.w;
+    }
+}
+
+__device__ __forceinline__ void store_row4(float* o, int x, int ix0, int ix1, const float* acc) {
+    if (x >= ix0 && x + 3 < ix1) {
+        *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (x + k >= ix0 && x + k < ix1) o[k] = acc[k];
+    }
+}
+
 // HA: load halo, TMAX*R rounded up to 4 (16-byte aligned box coordinates).
 template <int R, int TILE, int TMAX>
 struct TbLayout {
@@ -72,7 +128,10 @@ struct TbLayout {
     static constexpr size_t smem = 128 + 2 * static_cast<size_t>(SW) * SW * sizeof(float);
 };
 
-template <int R, int TILE, int TMAX>
+// RV: rows per thread visit (1, or 2: two stacked rows share their a0
+// neighbour loads -- each row's centre is the other's a0 neighbour -- and give
+// each thread twice the independent work)
+template <int R, int TILE, int TMAX, int RV = 1>
 __global__ void __launch_bounds__(256) diffusion_tb_kernel(const __grid_constant__ DiffusionTBArgs A) {
     using L = TbLayout<R, TILE, TMAX>;
     constexpr int SW = L::SW, HA = L::HA;
@@ -102,7 +161,8 @@ __global__ void __launch_bounds__(256) diffusion_tb_kernel(const __grid_constant
     // (Packed fp32x2 arithmetic as in the acoustic kernels measured 3 %
     // slower here in the sustained C1 run, 747 vs 769 GPts/s: scalar. The
     // 64-wide core tile is the measured best for radius 1: 48 / 56 / 72 / 80
-    // / 96 (SF_TB_TILE) ran at 699 / 714 / 677 / 654 / 599 vs 759 GPts/s.)
+    // / 96 (SF_TB_TILE) ran at 699 / 714 / 677 / 654 / 599 vs 759 GPts/s;
+    // two rows per visit (RV = 2) 776 vs 760.)
     // Each thread updates 4 consecutive a1 cells per visit: one aligned
     // (4 + 2RA)-float window (LDS.128s) gives every a1 neighbour, one
     // LDS.128 per a0 row offset gives the a0 neighbours of all four.
@@ -124,7 +184,48 @@ __global__ void __launch_bounds__(256) diffusion_tb_kernel(const __grid_constant
         const int xlo = max(grow, ix0) & ~3, xhi = min(SW - grow, ix1);
         const int x = 4 * lx;
         const bool col_on = ly < RPP && x + 3 >= xlo && x < xhi;
-        for (int y = ylo + ly; col_on && y < yhi; y += RPP) {
+        if (RV == 2) {
+            for (int y = ylo + 2 * ly; col_on && y < yhi; y += 2 * RPP) {
+                const bool two = y + 1 < yhi;
+                const float* c0p = in + y * SW + x;
+                const float* c1p = c0p + SW;
+                float win0[4 + 2 * RA], win1[4 + 2 * RA];
+                load_window<RA>(c0p, win0);
+                float4 up0[R], dn0[R];
+#pragma unroll
+                for (int j = 1; j <= R; ++j) {
+                    up0[j - 1] = *reinterpret_cast<const float4*>(c0p - j * SW);
+                    dn0[j - 1] = *reinterpret_cast<const float4*>(c0p + j * SW);
+                }
+                float acc[4];
+                diffusion_row4<R, RA>(A, win0, up0, dn0, acc);
+                store_row4(out + y * SW + x, x, ix0, ix1, acc);
+                if (two) {
+                    // row y+1: its window's centre is dn0[0]; a0 neighbours are
+                    // row y (win0's centre), up0 shifted by one, dn0 shifted
+                    // by one and one more row below
+#pragma unroll
+                    for (int q = 0; q < (4 + 2 * RA) / 4; ++q) {  // centre chunk = dn0[0]
+                        const float4 w = q == RA / 4 ? dn0[0]
+                                                     : *reinterpret_cast<const float4*>(c1p - RA + 4 * q);
+                        win1[4 * q] = w.x;
+                        win1[4 * q + 1] = w.y;
+                        win1[4 * q + 2] = w.z;
+                        win1[4 * q + 3] = w.w;
+                    }
+                    float4 up1[R], dn1[R];
+                    up1[0] = make_float4(win0[RA], win0[RA + 1], win0[RA + 2], win0[RA + 3]);
+#pragma unroll
+                    for (int j = 2; j <= R; ++j) up1[j - 1] = up0[j - 2];
+#pragma unroll
+                    for (int j = 1; j < R; ++j) dn1[j - 1] = dn0[j];
+                    dn1[R - 1] = *reinterpret_cast<const float4*>(c1p + R * SW);
+                    diffusion_row4<R, RA>(A, win1, up1, dn1, acc);
+                    store_row4(out + (y + 1) * SW + x, x, ix0, ix1, acc);
+                }
+            }
+        }
+        for (int y = ylo + ly; RV == 1 && col_on && y < yhi; y += RPP) {
             {
                 const float* c = in + y * SW + x;
                 float win[4 + 2 * RA];

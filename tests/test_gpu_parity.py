@@ -309,12 +309,15 @@ def test_diffusion_temporal_blocking_vs_oracle(sf, port, order, n, nt):
     assert_parity(b.u.data, ref)
 
 
-@pytest.mark.parametrize("tile", ["48", "56", "72", "80", "96"])
-def test_diffusion_tile_variants_vs_oracle(sf, port, monkeypatch, tile):
+@pytest.mark.parametrize("tile,rv", [("48", "1"), ("56", "1"), ("64", "1"), ("64", "2"),
+                                     ("72", "1"), ("80", "1"), ("96", "1")])
+def test_diffusion_tile_variants_vs_oracle(sf, port, monkeypatch, tile, rv):
     """Radius-1 temporal blocking with every selectable core tile
-    (SF_TB_TILE; 64 is the measured default) on a ragged grid."""
+    (SF_TB_TILE; 64 is the measured default) and one or two rows per thread
+    visit (SF_TB_RV; 2 is the default) on a ragged grid."""
     from fractions import Fraction
     monkeypatch.setenv("SF_TB_TILE", tile)
+    monkeypatch.setenv("SF_TB_RV", rv)
     n, nt = 301, 21
     rng = np.random.default_rng(int(tile))
     u = rng.random((2, n, n)).astype(np.float32)
