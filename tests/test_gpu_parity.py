@@ -682,3 +682,77 @@ def test_eta_zero_boxes_skipped_bitwise(sf, port, order):
         assert fractions[1] < fractions[0]  # the sponge leaves fewer
     finally:
         _lib.lib.sf_plan_destroy(plan)
+
+
+@pytest.mark.parametrize("order", [4, 8, 16])
+@pytest.mark.parametrize("forward", [True, False])
+def test_special_values_bitwise(sf, port, order, forward):
+    """Signed zeros, subnormals and near-limit magnitudes in the wavefield,
+    tiny m (reciprocals on the slow path) and subnormal eta: the kernels keep
+    IEEE semantics (no flush-to-zero, no contraction), so the result is still
+    bitwise the CPU oracle's. (NaN is excluded: its payload is not specified
+    by IEEE and differs between x86 and the GPU.)"""
+    shape = (30, 38, 70)
+    nt = 7
+    c = random_case(port, shape, order, seed=500 + order + forward)
+    rng = c["rng"]
+    u0 = (1e-3 * rng.standard_normal((3,) + shape)).astype(np.float32)
+    pick = rng.random((3,) + shape)
+    u0[pick < 0.15] = 0.0
+    u0[(pick >= 0.15) & (pick < 0.3)] = -0.0
+    sub = (pick >= 0.3) & (pick < 0.45)
+    u0[sub] = (rng.standard_normal(sub.sum()) * 1e-39).astype(np.float32)  # subnormals
+    big = (pick >= 0.45) & (pick < 0.47)
+    u0[big] = (rng.standard_normal(big.sum()) * 1e30).astype(np.float32)
+    m = c["m"].copy()
+    mp = rng.random(shape)
+    m[mp < 0.05] = 1e-30                       # t3 near the float range: slow reciprocal path
+    eta = c["eta"].copy()
+    eta[(mp >= 0.05) & (mp < 0.1)] = 1e-40     # subnormal damping
+    eta[(mp >= 0.1) & (mp < 0.15)] = -0.0
+    assert np.isfinite(u0).all()
+    src = rng.standard_normal((nt, 3)).astype(np.float32)
+    rec = rng.standard_normal((nt, 17)).astype(np.float32)
+    if forward:
+        s_in, r_in = src, np.zeros_like(rec)
+    else:
+        s_in, r_in = np.zeros_like(src), rec
+    out = run_plan_raw(sf, shape, order, forward, c["dt"], 10.0, nt, m, eta, s_in.copy(),
+                       c["src_ci"], c["src_w"], r_in.copy(), c["rec_ci"], c["rec_w"], u=u0.copy())
+    coefs = port.coefs(3, order, forward, c["dt"], 10.0)
+    u = u0.copy()
+    if forward:
+        r = r_in.copy()
+        port.acoustic_run(coefs, u, m, eta, s_in.copy(), c["src_ci"], c["src_w"], r, c["rec_ci"],
+                          c["rec_w"], nt)
+        got_tr, want_tr = out[6], r
+    else:
+        s = s_in.copy()
+        port.acoustic_run(coefs, u, m, eta, r_in.copy(), c["rec_ci"], c["rec_w"], s, c["src_ci"],
+                          c["src_w"], nt)
+        got_tr, want_tr = out[3], s
+    fin = np.isfinite(u)
+    assert np.array_equal(np.isfinite(out[0]), fin)
+    assert np.array_equal(bits(out[0])[fin], bits(u)[fin])
+    ok = np.isfinite(want_tr)
+    assert np.array_equal(bits(got_tr)[ok], bits(want_tr)[ok])
+
+
+def test_diffusion_special_values_bitwise(sf, port):
+    """Temporal blocking keeps subnormals and signed zeros (radius 1 and 4)."""
+    from fractions import Fraction
+    for order in (2, 8):
+        n, nt = 133, 17
+        rng = np.random.default_rng(900 + order)
+        u = rng.standard_normal((2, n, n)).astype(np.float32)
+        pick = rng.random((2, n, n))
+        u[pick < 0.2] = -0.0
+        u[(pick >= 0.2) & (pick < 0.5)] *= np.float32(1e-39)
+        cfg = sf.DiffusionConfig(nx=n, ny=n, alpha=Fraction(1, 3), dx=Fraction(1, n - 1),
+                                 dy=Fraction(1, n - 1), nt=nt, order=order)
+        b = sf.make_diffusion_operator(cfg)
+        b.u.data[...] = u
+        b.op.apply()
+        ref = u.copy()
+        port.diffusion_run(ref, order, (1, 3), (1, n - 1), nt)
+        assert np.array_equal(bits(b.u.data), bits(ref))
