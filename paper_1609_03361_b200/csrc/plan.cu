@@ -155,6 +155,8 @@ struct sf_plan {
     CUtensorMap tm_cur[3], tm_pme[3], tm_m, tm_eta;
     // FWI: history (nt+2 levels), adjoint slots v, gradient
     CUtensorMap tm_hist_cur, tm_hist_pme, tm_v_cur[3], tm_v_pme[3], tm_grad;
+    // the gradient kernel's own 64 x 8 boxes when the forward runs 8-warp tiles
+    CUtensorMap tm_m_g, tm_eta_g, tm_hist_pme_g, tm_v_cur_g[3], tm_v_pme_g[3];
     dim3 grid_grad;          // GRAD launches use 4-warp CTAs (6 boxes per stage)
     int zchunk_grad = 0;
     size_t smem_grad = 0;
@@ -711,11 +713,20 @@ void setup_tma(Plan& p) {
     make_tensor_map(&p.tm_m, p, p.m, tx, ty);
     make_tensor_map(&p.tm_eta, p, p.eta, tx, ty);
     if (p.kind == Plan::FWI) {
+        // forward (history levels): the stencil's tile; adjoint slots v and the
+        // gradient kernel's m / eta / u-history boxes: its fixed 64 x 8 tile
+        const uint32_t gty = 8, gcy = gty + static_cast<uint32_t>(2 * r);
         make_tensor_map(&p.tm_hist_cur, p, p.hist, wb, cy, p.nt + 2);
         make_tensor_map(&p.tm_hist_pme, p, p.hist, tx, ty, p.nt + 2);
+        make_tensor_map(&p.tm_hist_pme_g, p, p.hist, 64, gty, p.nt + 2);
+        make_tensor_map(&p.tm_m_g, p, p.m, 64, gty);
+        make_tensor_map(&p.tm_eta_g, p, p.eta, 64, gty);
+        const uint32_t gwb = 64 + 2 * static_cast<uint32_t>((r + 3) / 4 * 4);
         for (int s = 0; s < 3; ++s) {
             make_tensor_map(&p.tm_v_cur[s], p, p.v[s], wb, cy);
             make_tensor_map(&p.tm_v_pme[s], p, p.v[s], tx, ty);
+            make_tensor_map(&p.tm_v_cur_g[s], p, p.v[s], gwb, gcy);
+            make_tensor_map(&p.tm_v_pme_g[s], p, p.v[s], 64, gty);
         }
     }
     if (p.use_vecq) {
@@ -869,6 +880,9 @@ struct MapSel {
     const CUtensorMap* cur = nullptr;
     const CUtensorMap* pme = nullptr;
     int level = 0;
+    // the FWI gradient kernel's 64 x 8 boxes of the same buffer (v slots, history)
+    const CUtensorMap* cur_g = nullptr;
+    const CUtensorMap* pme_g = nullptr;
 };
 
 bool map_for(const Plan& p, const float* f, MapSel* m) {
@@ -878,14 +892,15 @@ bool map_for(const Plan& p, const float* f, MapSel* m) {
             return true;
         }
         if (p.v[s] && f == p.v[s]) {
-            *m = {&p.tm_v_cur[s], &p.tm_v_pme[s], 0};
+            *m = {&p.tm_v_cur[s], &p.tm_v_pme[s], 0, &p.tm_v_cur_g[s], &p.tm_v_pme_g[s]};
             return true;
         }
     }
     if (p.hist && f >= p.hist) {
         const int64_t d = f - p.hist;
         if (d % p.slot_elems == 0 && d / p.slot_elems < p.nt + 2) {
-            *m = {&p.tm_hist_cur, &p.tm_hist_pme, static_cast<int>(d / p.slot_elems)};
+            *m = {&p.tm_hist_cur, &p.tm_hist_pme, static_cast<int>(d / p.slot_elems), nullptr,
+                  &p.tm_hist_pme_g};
             return true;
         }
     }
@@ -908,7 +923,8 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
     MapSel mc, mp, mo, mu;
     const bool maps = p.use_tma && p.ndim == 3 && map_for(p, cur, &mc) && map_for(p, prev, &mp);
     const bool grad_ok =
-        !grad || (p.use_vec && !p.use_vecq && map_for(p, out, &mo) && map_for(p, uhist, &mu));
+        !grad || (p.use_vec && !p.use_vecq && map_for(p, out, &mo) && map_for(p, uhist, &mu) &&
+                  mc.cur_g && mp.pme_g && mo.pme_g && mu.pme_g);
     if (maps && grad_ok) {
         TmaStencilArgs T;
         std::memset(&T, 0, sizeof T);
@@ -949,9 +965,13 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
         for (int k = 0; k < 3; ++k) T.pk_tc[k] = f2_splat_host(T.tc[k]);
         T.pk_c0 = f2_splat_host(T.c0);
         for (int j = 0; j < 8; ++j) T.pk_cj[j] = f2_splat_host(T.cj[j]);
-        if (grad) {
-            T.old = *mo.pme;
-            T.uh = *mu.pme;
+        if (grad) {  // the gradient kernel's own 64 x 8 boxes of every buffer
+            T.cur = *mc.cur_g;
+            T.prev = *mp.pme_g;
+            T.old = *mo.pme_g;
+            T.uh = *mu.pme_g;
+            T.m = p.tm_m_g;
+            T.eta = p.tm_eta_g;
             T.lv_uh = mu.level;
             T.grad = p.tm_grad;
             T.gradp = grad;
@@ -1892,10 +1912,10 @@ void enable_tma(Plan& p) {
     const bool vec_on = !(vec && vec[0] == '0');
     if (vec_on && p.ac.radius <= 4) {
         p.use_vec = true;
-        // FWI: one set of maps serves the forward and the 4-warp gradient kernel
-        p.vec_warps = (p.ac.radius <= 3 || p.kind == Plan::FWI) ? 4 : 8;
-        if (const char* w = std::getenv("SF_VEC_WARPS"))
-            if (p.kind != Plan::FWI) p.vec_warps = std::atoi(w) == 4 ? 4 : 8;
+        // FWI: the forward runs the same tile choice as a plain forward plan;
+        // the 4-warp gradient kernel has its own maps (setup_tma)
+        p.vec_warps = p.ac.radius <= 3 ? 4 : 8;
+        if (const char* w = std::getenv("SF_VEC_WARPS")) p.vec_warps = std::atoi(w) == 4 ? 4 : 8;
         // tile width: 64 (16 lanes per row) unless 32-wide 4-warp tiles
         // cover the interior with fewer padded points (FWI: 64 wide, one set
         // of maps serves the forward and gradient kernels)
