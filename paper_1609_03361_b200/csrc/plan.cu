@@ -160,6 +160,7 @@ struct sf_plan {
     dim3 grid_grad;          // GRAD launches use 4-warp CTAs (6 boxes per stage)
     int zchunk_grad = 0;
     size_t smem_grad = 0;
+    int tma_stages_grad = 4;
     std::map<std::pair<int64_t, int64_t>, cudaGraphExec_t> graphs;
     std::vector<std::string> arg_names;
     std::vector<int64_t> arg_bytes;
@@ -768,8 +769,17 @@ void setup_tma(Plan& p) {
                                          static_cast<int>(p.tma_smem)));
         }
         if (p.kind == Plan::FWI) {
+            // the gradient kernel streams 6 boxes per stage and prefers a deeper
+            // pipeline than the forward (C5 adjoint: 4 stages 166 ms, 3 stages
+            // 174 ms per sweep); SF_TMA_STAGES_GRAD overrides
+            int gst = 4;
+            if (const char* env = std::getenv("SF_TMA_STAGES_GRAD")) {
+                const int v = std::atoi(env);
+                if (v >= 2 && v <= 12) gst = v;
+            }
+            p.tma_stages_grad = gst;
             make_tensor_map(&p.tm_grad, p, p.grad, 64, 8);
-            p.smem_grad = vec_smem_bytes(r, 4, stages, 6);
+            p.smem_grad = vec_smem_bytes(r, 4, gst, 6);
             SF_CUDA(cudaFuncSetAttribute(vec_grad_ptr(r), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(p.smem_grad)));
         }
@@ -966,6 +976,7 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
         T.pk_c0 = f2_splat_host(T.c0);
         for (int j = 0; j < 8; ++j) T.pk_cj[j] = f2_splat_host(T.cj[j]);
         if (grad) {  // the gradient kernel's own 64 x 8 boxes of every buffer
+            T.stages = p.tma_stages_grad;
             T.cur = *mc.cur_g;
             T.prev = *mp.pme_g;
             T.old = *mo.pme_g;
