@@ -756,3 +756,50 @@ def test_diffusion_special_values_bitwise(sf, port):
         ref = u.copy()
         port.diffusion_run(ref, order, (1, 3), (1, n - 1), nt)
         assert np.array_equal(bits(b.u.data), bits(ref))
+
+
+@pytest.mark.parametrize("order", [4, 8, 12])
+@pytest.mark.parametrize("forward", [True, False])
+def test_zero_eta_boxes_special_values(sf, port, order, forward):
+    """All-zero eta boxes (skipped loads, 0.0f operands) with signed-zero,
+    subnormal and infinite wavefield values and zero / negative-zero /
+    subnormal m (infinite or huge t3): still the CPU oracle's bits wherever
+    the result is finite, and the same non-finite pattern."""
+    shape = (44, 53, 100)
+    nt = 5
+    c = random_case(port, shape, order, seed=700 + order + 2 * forward)
+    rng = c["rng"]
+    eta = np.zeros(shape, np.float32)          # almost every box is +0.0
+    eta[:4] = c["eta"][:4]
+    m = c["m"].copy()
+    mp = rng.random(shape)
+    m[mp < 0.02] = 0.0
+    m[(mp >= 0.02) & (mp < 0.04)] = -0.0
+    m[(mp >= 0.04) & (mp < 0.06)] = 1e-40
+    m[(mp >= 0.06) & (mp < 0.08)] = 1e-30
+    u0 = (1e-3 * rng.standard_normal((3,) + shape)).astype(np.float32)
+    pick = rng.random((3,) + shape)
+    u0[pick < 0.2] = 0.0
+    u0[(pick >= 0.2) & (pick < 0.4)] = -0.0
+    sub = (pick >= 0.4) & (pick < 0.5)
+    u0[sub] = (rng.standard_normal(sub.sum()) * 1e-39).astype(np.float32)
+    u0[1, 20, 26, 50] = np.inf                 # a few infinities (they spread R planes per step)
+    u0[0, 30, 10, 80] = -np.inf
+    u0[2, 12, 40, 20] = np.inf
+    src = rng.standard_normal((nt, 3)).astype(np.float32)
+    rec = rng.standard_normal((nt, 17)).astype(np.float32)
+    s_in, r_in = (src, np.zeros_like(rec)) if forward else (np.zeros_like(src), rec)
+    out = run_plan_raw(sf, shape, order, forward, c["dt"], 10.0, nt, m, eta, s_in.copy(),
+                       c["src_ci"], c["src_w"], r_in.copy(), c["rec_ci"], c["rec_w"], u=u0.copy())
+    coefs = port.coefs(3, order, forward, c["dt"], 10.0)
+    u = u0.copy()
+    if forward:
+        port.acoustic_run(coefs, u, m, eta, s_in.copy(), c["src_ci"], c["src_w"], r_in.copy(),
+                          c["rec_ci"], c["rec_w"], nt)
+    else:
+        port.acoustic_run(coefs, u, m, eta, r_in.copy(), c["rec_ci"], c["rec_w"], s_in.copy(),
+                          c["src_ci"], c["src_w"], nt)
+    fin = np.isfinite(u)
+    assert np.array_equal(np.isfinite(out[0]), fin)
+    assert np.array_equal(bits(out[0])[fin], bits(u)[fin])
+    assert (~fin).any() and fin.sum() > 0.2 * fin.size
