@@ -2741,6 +2741,10 @@ int sf_slab_chain_run(sf_plan* const* plans, int nplans, int64_t b, int64_t e) {
                 throw Status(SF_ERR_INVALID, "chain slabs must be adjacent and ordered");
         }
         if (b < 0 || e > plans[0]->nt || b > e) throw Status(SF_ERR_INVALID, "step range");
+        for (int i = 0; i < nplans; ++i) {  // all-zero eta boxes of each slab (its own planes)
+            SF_CUDA(cudaSetDevice(plans[i]->device));
+            sfb::ensure_eta_flags(*plans[i]);
+        }
         for (int64_t k = b; k < e; ++k) sfb::chain_step(plans, nplans, k);
         for (int i = 0; i < nplans; ++i) sfb::check_kernel_errors(*plans[i]);
     });

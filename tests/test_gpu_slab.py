@@ -15,13 +15,15 @@ def bits(a):
     return np.ascontiguousarray(a).view(np.uint32)
 
 
-@pytest.mark.parametrize("order,forward,nslabs", [(4, True, 3), (8, False, 2), (2, True, 4),
-                                                  (16, True, 2)])
-def test_slab_chain_matches_single_domain(port, order, forward, nslabs):
+@pytest.mark.parametrize("order,forward,nslabs,shape", [
+    (4, True, 3, (67, 40, 45)), (8, False, 2, (67, 40, 45)), (2, True, 4, (67, 40, 45)),
+    (16, True, 2, (67, 40, 45)),
+    # wide enough laterally for all-zero eta boxes (skipped loads) in every slab
+    (4, True, 3, (67, 60, 140)), (8, False, 2, (58, 70, 140)), (12, True, 2, (58, 60, 140))])
+def test_slab_chain_matches_single_domain(port, order, forward, nslabs, shape):
     import paper_1609_03361_b200 as sf
     from paper_1609_03361_b200.slab import SlabPartition, SlabRun, assemble, chain_run
     from test_gpu_parity import run_plan_raw
-    shape = (67, 40, 45)
     nt = 20
     r = order // 2
     rng = np.random.default_rng(order)
@@ -33,11 +35,12 @@ def test_slab_chain_matches_single_domain(port, order, forward, nslabs):
     pts = []
     for b in bounds:
         for dz in (-1.3, -0.4, 0.2, 0.9):
-            pts.append([(b + dz) * 10.0, rng.uniform(r + 1, 38 - r) * 10.0,
-                        rng.uniform(r + 1, 43 - r) * 10.0])
+            pts.append([(b + dz) * 10.0, rng.uniform(r + 1, shape[1] - 2 - r) * 10.0,
+                        rng.uniform(r + 1, shape[2] - 2 - r) * 10.0])
     for _ in range(6):
-        pts.append([rng.uniform(r + 1, 65 - r) * 10.0, rng.uniform(r + 1, 38 - r) * 10.0,
-                    rng.uniform(r + 1, 43 - r) * 10.0])
+        pts.append([rng.uniform(r + 1, shape[0] - 2 - r) * 10.0,
+                    rng.uniform(r + 1, shape[1] - 2 - r) * 10.0,
+                    rng.uniform(r + 1, shape[2] - 2 - r) * 10.0])
     pts = np.array(pts)
     src_c, rec_c = pts[::2], pts[1::2]
     src_ci, src_w = port.interp(src_c, 10.0, shape)
@@ -54,6 +57,13 @@ def test_slab_chain_matches_single_domain(port, order, forward, nslabs):
     slabs = [SlabRun(SlabPartition.split(shape[0], r, nslabs, g), shape, order, forward, nt, dt,
                      10.0, m, eta, src, src_ci, src_w, rec, rec_ci, rec_w) for g in range(nslabs)]
     chain_run(slabs, 0, nt)
+    if shape[2] >= 140:  # the wide cases: every slab skipped some all-zero eta boxes
+        import ctypes as C
+        from paper_1609_03361_b200 import _lib
+        for sl in slabs:
+            frac = C.c_double()
+            assert _lib.lib.sf_plan_eta_skip_fraction(sl.plan, C.byref(frac)) == 0
+            assert frac.value > 0.0
     u, s_tr, r_tr = assemble(slabs, shape, nt, ns, nr)
     assert np.abs(ref[0]).max() > 0
     assert np.array_equal(bits(u), bits(ref[0]))
