@@ -1,24 +1,31 @@
 """Benchmark of the B200 stencil hot path (contract: one JSON line on rank 0).
 
-Workload (default): BASELINE.json configs[1] (SURVEY "C2"), the 3D acoustic
-forward at space order 4 on 281^3 (201^3 + 40-point damping layer on every
-face), 10 m spacing, two layers 1.5/2.5 km/s, 10 Hz Ricker source at depth
-20 m, 101 receivers on a line, 1000 ms at dt = 0.4 h / vmax = 1.6 ms
-(625 steps). A benchmark "step" is one full apply of that operator: 625 time
-steps of stencil + injection + sampling, i.e. 277^3 * 625 = 1.328e10
-interior grid-point updates.
+Default workload: SURVEY C4 at one GPU -- the largest single-GPU config of
+BASELINE.json: 3D acoustic forward, space order 8, 1024^3 (40-point damping
+layer on every face), 10 m spacing, seeded smooth random velocity in
+[1.5, 4.5] km/s (Gaussian-filtered noise, sigma 8 cells, generated on the GPU
+from global indices: csrc/medium.cu), 8 Ricker sources at seeded random
+positions, 101 receivers, 1000 time steps at dt = 0.4 h / vmax. With
+`--gpus N` (torchrun) the grid is N such blocks stacked in depth
+((1024 N) x 1024 x 1024), one depth slab per GPU, r-deep halos exchanged over
+NCCL every step, each rank generating only its own slab's medium (weak
+scaling). `--config` selects the other BASELINE configs (c1 diffusion, c2,
+c3o4..c3o16, c5 FWI). A bench "step" is one full apply: all nt time steps of
+stencil + injection + sampling.
 
   value : GPts/s with every buffer resident in HBM (sf_plan_run, CUDA graph),
           device-timed with CUDA events, max over ranks.
-  e2e   : GPts/s through the C-ABI entry sf_acoustic_apply with host (pinned)
-          buffers: H2D of all nine arguments, the 625 steps, D2H of the three
-          field slots and both traces, every step.
+  e2e   : GPts/s through the C-ABI entry sf_plan_invoke (Operator.apply)
+          with pinned host buffers: H2D of all nine arguments, the nt steps,
+          D2H of the three field slots and the traces, every step.
   roofline : the stencil kernel's algorithmic bytes (20 B per interior point:
-          read u(t), u(t-1), m, eta, write u(t+1)) / its average launch time.
+          read u(t), u(t-1), m, eta, write u(t+1), less the all-zero eta
+          boxes the kernel skips) / its average launch time.
 
-`--impl reference` times the reference's own CPU implementation (the
-stencilforge library compiled from its sources into oracle/_ref, generated
-C/OpenMP kernel via Operator::apply) on a bounded sample of the same workload.
+`--impl reference` times the reference's own CPU implementation (stencilforge
+compiled from its sources into oracle/_ref: acoustic_build + the JIT'd
+C/OpenMP Operator::apply) on a bounded sample of the same workload. That arm
+never imports this package (it uses only oracle/ through tests/oracle_lib).
 """
 from __future__ import annotations
 
@@ -29,35 +36,74 @@ import subprocess
 import sys
 import threading
 import time
+from types import SimpleNamespace
 
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+SMOOTH = dict(seed=1234, sigma=8.0, v_lo=1500.0, v_hi=4500.0, v_min=1500.0)
+
 CONFIGS = {
+    # SURVEY C4 at one GPU (default): the 1024^3 per-GPU block, order 8, 8 sources
+    "c4": dict(shape=(1024, 1024, 1024), order=8, nt=1000, nsrc=8, recs="line"),
     # SURVEY C1 / BASELINE configs[0]: 2D diffusion, exact 1/4 weights
     "c1": dict(kind="diffusion", n=2048, nt=500, order=2),
-    # SURVEY C4 at one GPU: the 1024^3 per-GPU slab, order 8, 8 sources
-    "c4": dict(shape=(1024, 1024, 1024), order=8, nt=1000, boundary=40, spacing=10.0,
-               random=True, smooth="sines", nsrc=8),
     # FWI gradient, forward with full history + adjoint/gradient
-    "c5": dict(kind="fwi", shape=(301, 301, 301), order=8, nt=1000, boundary=40, spacing=10.0),
-    # SURVEY C2 / BASELINE configs[1]
-    "c2": dict(shape=(281, 281, 281), order=4, nt=625, boundary=40, spacing=10.0,
-               v_top=1500.0, v_bottom=2500.0, random=False),
-    # SURVEY C3 / BASELINE configs[2] (one order per run)
-    "c3o4": dict(shape=(512, 512, 512), order=4, nt=500, boundary=40, spacing=10.0,
-                 random=True),
-    "c3o6": dict(shape=(512, 512, 512), order=6, nt=500, boundary=40, spacing=10.0,
-                 random=True),
-    "c3o8": dict(shape=(512, 512, 512), order=8, nt=500, boundary=40, spacing=10.0,
-                 random=True),
-    "c3o12": dict(shape=(512, 512, 512), order=12, nt=500, boundary=40, spacing=10.0,
-                  random=True),
-    "c3o16": dict(shape=(512, 512, 512), order=16, nt=500, boundary=40, spacing=10.0,
-                  random=True),
+    "c5": dict(kind="fwi", shape=(301, 301, 301), order=8, nt=1000),
+    # SURVEY C2 / BASELINE configs[1]: two layers 1.5 / 2.5 km/s
+    "c2": dict(shape=(281, 281, 281), order=4, nt=625, layered=True),
+    # SURVEY C3 / BASELINE configs[2] (one order per run), 256 x 256 receivers
+    **{f"c3o{o}": dict(shape=(512, 512, 512), order=o, nt=500, recs="surface")
+       for o in (4, 6, 8, 12, 16)},
 }
+BW, H = 40, 10.0
+
+
+def workload(name, world=1, stable_dt=None):
+    """The acoustic workload of a config, global over `world` depth blocks.
+    stable_dt(order, v_max) -> seconds is supplied by the caller (the product's
+    or the reference's own AcousticModel::stable_dt), so this function needs
+    neither implementation."""
+    c = CONFIGS[name]
+    block = tuple(c["shape"])
+    shape = (block[0] * world,) + block[1:]
+    order, nt = c["order"], c["nt"]
+    r = order // 2
+    mid = block[1] // 2
+    w = SimpleNamespace(name=name, block=block, shape=shape, order=order, nt=nt, bw=BW, h=H,
+                        f0=10.0, world=world)
+    if c.get("layered"):
+        w.v_top, w.v_bottom, w.smooth = 1500.0, 2500.0, None
+        w.dt = 0.4 * H / 2500.0
+        w.src_coords = [[(BW + 2) * H, mid * H, mid * H]]
+        w.rec_coords = [[(BW + 2) * H, mid * H, (BW + 2 * i) * H] for i in range(101)]
+        return w
+    w.v_top = w.v_bottom = 4500.0
+    w.smooth = dict(SMOOTH, shape=shape, boundary_width=BW, spacing=H)
+    w.dt = min(0.4 * H / 4500.0, stable_dt(order, 4500.0))
+    if c.get("nsrc", 1) > 1:  # C4: seeded random interior source positions (global grid)
+        rng = np.random.default_rng(8)
+        w.src_coords = [[rng.uniform(BW + r, e - BW - r - 1) * H for e in shape]
+                        for _ in range(c["nsrc"])]
+    else:
+        w.src_coords = [[(BW + 2) * H, mid * H, mid * H]]
+    if c.get("recs") == "line":
+        w.rec_coords = [[(BW + 10) * H, (BW + 2 + 7.3 * i) * H, mid * H] for i in range(101)]
+    else:
+        lo, hi = (BW + 2) * H, (block[1] - BW - 3) * H
+        g = np.linspace(lo + 0.37 * H, hi - 0.41 * H, 256)
+        w.rec_coords = [[(BW + 10) * H, y, z] for y in g for z in g]
+    return w
+
+
+def interior_points(shape, order):
+    r = order // 2
+    n = 1
+    for e in shape:
+        n *= e - 2 * r
+    return n
 
 
 def load_peaks():
@@ -65,83 +111,29 @@ def load_peaks():
     try:
         with open(path) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def smooth_velocity(shape, seed, sigma=8.0, vmin=1500.0, vmax=4500.0):
-    """Seeded N(0,1) noise, separable Gaussian filter (sigma cells, truncate
-    4 sigma, reflect), affinely rescaled to [vmin, vmax]."""
-    from scipy.ndimage import gaussian_filter
-    rng = np.random.default_rng(seed)
-    noise = rng.standard_normal(shape, dtype=np.float32)
-    f = gaussian_filter(noise, sigma=sigma, mode="reflect", truncate=4.0)
-    lo, hi = float(f.min()), float(f.max())
-    return vmin + (vmax - vmin) * (f.astype(np.float64) - lo) / (hi - lo)
-
-
-def smooth_velocity_sines(shape, seed, vmin=1500.0, vmax=4500.0, modes=6):
-    """Cheap smooth random velocity for very large grids (C4): a seeded sum
-    of separable sinusoids with wavelengths >= 40 cells, rescaled to
-    [vmin, vmax]. Built per plane (float64 only for one plane at a time)."""
-    rng = np.random.default_rng(seed)
-    n0, n1, n2 = shape
-    k = rng.uniform(2 * np.pi / 200, 2 * np.pi / 40, (modes, 3))
-    ph = rng.uniform(0, 2 * np.pi, (modes, 3))
-    amp = rng.uniform(0.5, 1.0, modes)
-    f1 = [np.cos(k[i, 1] * np.arange(n1) + ph[i, 1]) for i in range(modes)]
-    f2 = [np.cos(k[i, 2] * np.arange(n2) + ph[i, 2]) for i in range(modes)]
-    f0 = [np.cos(k[i, 0] * np.arange(n0) + ph[i, 0]) for i in range(modes)]
-    tot = float(amp.sum())
-    v = np.empty(shape, np.float64)
-    for a in range(n0):
-        pl = np.zeros((n1, n2))
-        for i in range(modes):
-            pl += amp[i] * f0[i][a] * np.outer(f1[i], f2[i])
-        v[a] = vmin + (vmax - vmin) * (pl / tot + 1.0) * 0.5
-    return v
-
-
-def make_model(cfg_name):
-    import paper_1609_03361_b200 as sf
-    c = CONFIGS[cfg_name]
-    shape = c["shape"]
-    bw, h = c["boundary"], c["spacing"]
-    if not c["random"]:
-        vmax = max(c["v_top"], c["v_bottom"])
-        model = sf.AcousticModel(shape=shape, boundary_width=bw, spacing=h, nt=c["nt"],
-                                 space_order=c["order"], f0=10.0, v_top=c["v_top"],
-                                 v_bottom=c["v_bottom"])
-        model.dt = 0.4 * h / vmax
-        mid = shape[1] // 2
-        model.src_coords = [[(bw + 2) * h, mid * h, mid * h]]
-        model.rec_coords = [[(bw + 2) * h, mid * h, (bw + 2 * i) * h] for i in range(101)]
-        return model, None, None
-    model = sf.AcousticModel(shape=shape, boundary_width=bw, spacing=h, nt=c["nt"],
-                             space_order=c["order"], f0=10.0, v_top=4500.0, v_bottom=4500.0)
-    model.dt = min(0.4 * h / 4500.0, model.stable_dt())
-    mid = shape[1] // 2
-    if c.get("nsrc", 1) > 1:  # C4: seeded random interior source positions
-        rng = np.random.default_rng(8)
-        r = c["order"] // 2
-        model.src_coords = [[rng.uniform(bw + r, e - bw - r - 1) * h for e in shape]
-                            for _ in range(c["nsrc"])]
-        model.rec_coords = [[(bw + 10) * h, (bw + 2 + 7.3 * i) * h, mid * h] for i in range(101)]
-        return model, smooth_velocity_sines(shape, 1234), 1500.0
-    model.src_coords = [[(bw + 2) * h, mid * h, mid * h]]
-    lo, hi = (bw + 2) * h, (shape[1] - bw - 3) * h
-    g = np.linspace(lo + 0.37 * h, hi - 0.41 * h, 256)
-    model.rec_coords = [[(bw + 10) * h, y, z] for y in g for z in g]
-    return model, smooth_velocity(shape, 1234), 1500.0
-
-
-def interior_points(model):
-    r = model.space_order // 2
-    n = 1
-    for e in model.shape:
-        n *= e - 2 * r
-    return n
+def cpu_info():
+    model, phys = None, set()
+    try:
+        with open("/proc/cpuinfo") as f:
+            cur = {}
+            for ln in f:
+                if ":" in ln:
+                    k, v = [x.strip() for x in ln.split(":", 1)]
+                    cur[k] = v
+                    if k == "model name":
+                        model = v
+                elif cur:
+                    phys.add((cur.get("physical id"), cur.get("core id")))
+                    cur = {}
+    except OSError:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count(),
+            "physical_cores": len(phys) if phys and None not in next(iter(phys)) else None}
 
 
 class ClockSampler:
@@ -201,16 +193,18 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def dist_init(args):
+def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
+
+
+def dist_start(local):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
 
 def barrier(world):
@@ -219,246 +213,328 @@ def barrier(world):
         dist.barrier()
 
 
-def max_over_ranks(world, value):
+def reduce_over_ranks(world, value, op="max"):
     if world == 1:
         return value
     import torch
     import torch.distributed as dist
     t = torch.tensor([value], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.MIN)
     return float(t.item())
 
 
-def cpu_reference_sample(model, cfg_name, v_field, v_min, steps=1, warmup=1, budget_s=20.0):
-    """The reference's CPU path (oracle/_ref: stencilforge JIT kernel) on a
-    bounded sample: the full grid for nt_s time steps. Returns GPts/s."""
-    # SURVEY 8(d) CPU protocol: all host threads, pinned close to cores
-    # (read by libgomp when the reference library loads it)
-    os.environ.setdefault("OMP_PROC_BIND", "close")
-    os.environ.setdefault("OMP_PLACES", "cores")
+# ---------------------------------------------------------------------------
+# The reference's CPU path (oracle/_ref, else the C port): never imports the
+# B200 package.
+
+def _oracle():
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_lib as ol
-    if ol.have_ref():
-        ref = ol.Ref()
-        kind = "reference"
-        threads = ref.max_threads()
-        ref.set_threads(threads)
-        case = ol.AcousticCase(shape=model.shape, nt=1, boundary_width=model.boundary_width,
-                               spacing=model.spacing, dt=model.dt, space_order=model.space_order,
-                               f0=model.f0, v_top=model.v_top, v_bottom=model.v_bottom,
-                               src_coords=model.src_coords, rec_coords=model.rec_coords)
-        # calibrate: time a short run, then size the sample to the budget
-        def timed(nt_s):
-            case.nt = nt_s
-            op = ol.ref_acoustic(ref, case, True)
-            if v_field is not None:
-                port = ol.Port()
-                m, eta = port.medium_from_velocity(v_field, model.boundary_width, model.spacing,
-                                                   v_min)
-                op.set("m", m)
-                op.set("eta", eta)
-            op.build()
-            t0 = time.perf_counter()
-            op.apply()
-            return time.perf_counter() - t0
-        t_cal = timed(4)
-        nt_s = int(max(4, min(model.nt, budget_s / max(t_cal / 4, 1e-6))))
-        for _ in range(warmup):
-            timed(min(nt_s, 4))
-        times = [timed(nt_s) for _ in range(max(1, steps))]
-        secs = float(np.median(times))
-    else:
+    return ol
+
+
+def _ref_threads():
+    # SURVEY 8(d) CPU protocol: all host threads, pinned close to cores (read
+    # by libgomp when the reference library loads it)
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
+
+
+def ref_acoustic_sample(w, budget_s, runs, warmup, forward_adjoint=False):
+    """Median GPts/s of `runs` applies of the reference's acoustic operator
+    (acoustic_build + Operator::apply, JIT'd OpenMP C, JIT excluded) on the
+    workload's first depth block, nt_s time steps each (nt_s sized so that
+    warmup + runs applies take about budget_s). forward_adjoint: each apply
+    is the forward operator then the adjoint one (FWI's two sweeps, the
+    gradient product itself excluded: the reference has none)."""
+    _ref_threads()
+    ol = _oracle()
+    shape = w.block  # the reference has no decomposition: one block
+    pts = interior_points(shape, w.order)
+    if not ol.have_ref():
+        raise RuntimeError("oracle/_ref/libsf_ref.so missing")
+    ref = ol.Ref()
+    threads = ref.max_threads()
+    ref.set_threads(threads)
+    medium = None
+    t_med = None
+    if w.smooth is not None:
         port = ol.Port()
-        kind = "port"
-        import multiprocessing
-        threads = multiprocessing.cpu_count()
-        nt_s = 8
-        m = np.zeros(model.shape, np.float32)
-        eta = np.zeros_like(m)
-        c = port.coefs(3, model.space_order, True, model.dt, model.spacing)
-        u = np.zeros((3,) + tuple(model.shape), np.float32)
-        src_ci, src_w = port.interp(np.array(model.src_coords), model.spacing, model.shape)
-        rec_ci, rec_w = port.interp(np.array(model.rec_coords), model.spacing, model.shape)
-        src = np.ones((nt_s, len(src_ci)), np.float32)
-        rec = np.zeros((nt_s, len(rec_ci)), np.float32)
         t0 = time.perf_counter()
-        port.acoustic_run(c, u, m + 1.0, eta, src, src_ci, src_w, rec, rec_ci, rec_w, nt_s)
-        secs = time.perf_counter() - t0
-    gpts = interior_points(model) * nt_s / secs / 1e9
-    sample = (f"{cfg_name} grid {'x'.join(map(str, model.shape))} order {model.space_order}, "
-              f"{nt_s} of {model.nt} time steps, median of {max(1, steps)} applies after "
-              f"{warmup} warm-up, JIT excluded, OMP_PROC_BIND={os.environ.get('OMP_PROC_BIND')} "
+        lo, hi = port.smooth_extrema(shape, 0, shape[0], w.smooth["seed"], w.smooth["sigma"])
+        medium = port.smooth_medium(shape, 0, shape[0], w.smooth["seed"], lo, hi,
+                                    sigma=w.smooth["sigma"], v_lo=w.smooth["v_lo"],
+                                    v_hi=w.smooth["v_hi"], boundary_width=w.bw, spacing=w.h,
+                                    v_min=w.smooth["v_min"])
+        t_med = time.perf_counter() - t0
+    # sources / receivers of the block (the slab workload keeps them in block 0)
+    src = [c for c in w.src_coords if c[0] < (shape[0] - 1) * w.h] or w.src_coords[:1]
+
+    def build(nt_s, forward=True):
+        case = ol.AcousticCase(shape=shape, nt=nt_s, boundary_width=w.bw, spacing=w.h, dt=w.dt,
+                               space_order=w.order, f0=w.f0, v_top=w.v_top,
+                               v_bottom=w.v_bottom, src_coords=src, rec_coords=w.rec_coords)
+        op = ol.ref_acoustic(ref, case, forward)
+        if medium is not None:
+            op.set("m", medium[0])
+            op.set("eta", medium[1])
+        op.build()
+        return op
+
+    def apply_all(ops):
+        t0 = time.perf_counter()
+        for o in ops:
+            o.apply()
+        return time.perf_counter() - t0
+
+    ops = [build(1, True)] + ([build(1, False)] if forward_adjoint else [])
+    apply_all(ops)
+    t1 = apply_all(ops)
+    nt_s = int(max(1, min(w.nt, round(budget_s / max(1, runs + warmup) / max(t1, 1e-6)))))
+    if nt_s > 1:
+        ops.clear()  # free the calibration operators' buffers first
+        ops = [build(nt_s, True)] + ([build(nt_s, False)] if forward_adjoint else [])
+    for _ in range(warmup):
+        apply_all(ops)
+    times = [apply_all(ops) for _ in range(max(1, runs))]
+    secs = float(np.median(times))
+    upd = pts * nt_s * (2 if forward_adjoint else 1)
+    what = "forward + adjoint operators" if forward_adjoint else "forward operator"
+    sample = (f"reference {what} (acoustic_build + Operator::apply, JIT'd C/OpenMP, JIT "
+              f"excluded) on {'x'.join(map(str, shape))} order {w.order}, {nt_s} of {w.nt} "
+              f"time steps per apply, median of {len(times)} applies after {warmup} warm-up"
+              + (f"; medium from the oracle's smooth-medium restatement ({t_med:.1f} s, "
+                 "untimed)" if t_med is not None else "")
+              + f"; OMP_PROC_BIND={os.environ.get('OMP_PROC_BIND')} "
               f"OMP_PLACES={os.environ.get('OMP_PLACES')}")
-    return {"value": gpts, "unit": "GPts/s", "cores": threads, "kind": kind, "sample": sample}
+    return {"value": upd / secs / 1e9, "unit": "GPts/s", "cores": threads, "kind": "reference",
+            "sample": sample, "cpu": cpu_info(), "runs_s": times}
 
 
-def run_reference_arm(args, world, rank):
-    if rank != 0:
-        return
-    if CONFIGS[args.config].get("kind") == "diffusion":
-        c = CONFIGS[args.config]
-        base = cpu_diffusion_sample(c["n"], c["nt"], args.cpu_budget)
-        pts = (c["n"] - 2) ** 2
-        print(json.dumps({"impl": "reference", "metric": "GPts/s (grid-point updates/sec)",
-                          "value": base["value"], "unit": "GPts/s", "n_gpus": world,
-                          "steps": args.steps, "warmup": args.warmup,
-                          "ms_per_step": pts * c["nt"] / (base["value"] * 1e9) * 1e3,
-                          "higher_is_better": True,
-                          "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-                          "data": "synthetic", "config": diffusion_config_block(c),
-                          "cpu_baseline": base,
-                          "e2e": {"value": base["value"], "unit": "GPts/s",
-                                  "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
-              flush=True)
-        return
-    if CONFIGS[args.config].get("kind") == "fwi":
-        print(json.dumps({"impl": "reference", "unavailable":
-                          "the reference has no FWI gradient (SPEC.md:635,639)"}), flush=True)
-        return
-    model, v, vmin = make_model(args.config)
-    base = cpu_reference_sample(model, args.config, v, vmin, steps=args.steps,
-                                warmup=args.warmup, budget_s=args.cpu_budget)
-    line = {
-        "impl": "reference", "metric": "GPts/s (grid-point updates/sec)", "value": base["value"],
-        "unit": "GPts/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        # one bench step = one full apply (all nt time steps) at the sampled rate
-        "ms_per_step": interior_points(model) * model.nt / (base["value"] * 1e9) * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic",
-        "config": config_block(args, model),
-        "cpu_baseline": base,
-        "e2e": {"value": base["value"], "unit": "GPts/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+def ref_diffusion_sample(n, nt, budget_s, runs, warmup):
+    _ref_threads()
+    ol = _oracle()
+    rng = np.random.default_rng(2016)
+    u0 = np.zeros((n, n), np.float32)
+    u0[1:-1, 1:-1] = rng.random((n - 2, n - 2))
+    ref = ol.Ref()
+    threads = ref.max_threads()
+    ref.set_threads(threads)
+
+    def build(k):
+        op = ol.ref_diffusion(ref, n, n, (1, 2), (1, n - 1), k, 2)
+        op.set("u", np.stack([u0, u0]))
+        op.build()
+        return op
+    op = build(10)
+    op.apply()
+    t = time.perf_counter()
+    op.apply()
+    cal = (time.perf_counter() - t) / 10
+    k = int(max(10, min(nt, budget_s / max(1, runs + warmup) / max(cal, 1e-9))))
+    op = build(k)
+    for _ in range(warmup):
+        op.apply()
+    times = []
+    for _ in range(max(1, runs)):
+        t = time.perf_counter()
+        op.apply()
+        times.append(time.perf_counter() - t)
+    secs = float(np.median(times))
+    return {"value": (n - 2) ** 2 * k / secs / 1e9, "unit": "GPts/s", "cores": threads,
+            "kind": "reference", "cpu": cpu_info(), "runs_s": times,
+            "sample": f"reference diffusion operator on {n}^2, {k} of {nt} steps per apply, "
+                      f"median of {len(times)} applies after {warmup} warm-up, JIT excluded"}
+
+
+def config_block(w, parallelism):
+    d = {"workload": f"{w.name}: 3D acoustic forward, space order {w.order}, "
+                     f"{'x'.join(map(str, w.shape))} (boundary {w.bw}), {w.nt} time steps, "
+                     f"dt {w.dt:.6g} s, {len(w.src_coords)} source(s), "
+                     f"{len(w.rec_coords)} receivers",
+         "grid": list(w.shape), "space_order": w.order, "nt": w.nt,
+         "interior_points": interior_points(w.shape, w.order), "parallelism": parallelism,
+         "bench_step": f"one full apply = {w.nt} time steps",
+         "medium": ("two layers 1.5 / 2.5 km/s (build_medium)" if w.smooth is None else
+                    f"seeded smooth random v in [1.5, 4.5] km/s: Gaussian-filtered hash noise, "
+                    f"sigma {w.smooth['sigma']:g} cells, seed {w.smooth['seed']} "
+                    "(csrc/medium.cu), sponge as build_medium"),
+         "l2": "working set (3 u slots + m + eta) larger than the 126 MB L2; no flush needed"}
+    return d
 
 
 def diffusion_config_block(c):
     n, nt = c["n"], c["nt"]
     return {"workload": f"c1: 2D diffusion {n}^2, order 2, {nt} steps, alpha 1/2, "
                         f"dx 1/{n - 1}, dt = dx^2/4", "interior_points": (n - 2) ** 2,
+            "bench_step": f"one full apply = {nt} time steps",
             "l2": "2 x 16 MiB slots are L2-resident (126 MB L2); HBM roofline is "
                   "a lower bound here"}
 
 
-def config_block(args, model):
+def ref_stable_dt():
+    ol = _oracle()
+    ref = ol.Ref()
+
+    def f(order, vmax):
+        return ref.lib.sfref_acoustic_stable_dt(3, np.array([64, 64, 64], np.int64), H, order,
+                                                vmax, vmax)
+    return f
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return
     c = CONFIGS[args.config]
-    return {"workload": f"{args.config}: 3D acoustic forward, space order {model.space_order}, "
-                        f"{'x'.join(map(str, model.shape))} (boundary {c['boundary']}), "
-                        f"{model.nt} time steps, dt {model.dt:.6g} s, "
-                        f"{len(model.rec_coords)} receivers",
-            "grid": list(model.shape), "space_order": model.space_order, "nt": model.nt,
-            "interior_points": interior_points(model), "parallelism": f"replicas{args.gpus}",
-            "l2": "working set (3 u slots + m + eta) larger than the 126 MB L2; no flush needed"}
+    budget = args.ref_budget
+    if c.get("kind") == "diffusion":
+        base = ref_diffusion_sample(c["n"], c["nt"], budget, args.steps, args.warmup)
+        pts = (c["n"] - 2) ** 2
+        cfg = diffusion_config_block(c)
+        ms = pts * c["nt"] / (base["value"] * 1e9) * 1e3
+    else:
+        w = workload(args.config, world, ref_stable_dt())
+        fwi = c.get("kind") == "fwi"
+        base = ref_acoustic_sample(w, budget, args.steps, args.warmup, forward_adjoint=fwi)
+        pts = interior_points(w.block, w.order)
+        cfg = config_block(w, f"reference CPU (one block of the {world}-GPU job)"
+                           if world > 1 else "reference CPU")
+        if fwi:
+            cfg["workload"] = (f"c5: FWI forward + adjoint sweeps 301^3 order 8, {w.nt} steps "
+                               "(the reference has no gradient: its two operators are timed)")
+        ms = pts * w.nt * (2 if fwi else 1) / (base["value"] * 1e9) * 1e3
+    line = {
+        "impl": "reference", "metric": "GPts/s (grid-point updates/sec)", "value": base["value"],
+        "unit": "GPts/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic", "config": cfg,
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu")},
+        "e2e": {"value": base["value"], "unit": "GPts/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    # the reference arm must not have touched the product (driver check)
+    assert "paper_1609_03361_b200" not in sys.modules, "reference arm imported the product"
+    print(json.dumps(line), flush=True)
 
 
-def run_b200_arm(args, world, rank, local):
-    import paper_1609_03361_b200 as sf
-    model, v, vmin = make_model(args.config)
-    setup = sf.acoustic_build(model, True, device=local, v_field=v, v_min=vmin, pinned=True)
-    op = setup.op
-    pts = interior_points(model)
-    r = model.space_order // 2
-    # resident: upload once, warm up (graph capture + clocks), then time
-    op.upload()
-    for _ in range(args.warmup):
-        op.run(0, model.nt)
-    op.synchronize()
-    tot_ms, sten_ms, launches_per_run = op.time(stencil=True)
-    import torch
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
-    barrier(world)
-    with ClockSampler(local) as clocks:
-        evs = []
-        torch.cuda.synchronize()
-        barrier(world)
-        t_wall = time.perf_counter()
-        total = 0.0
-        for _ in range(args.steps):
-            t, _, _ = op.time(stencil=False)
-            total += t
-        torch.cuda.synchronize()
-        t_wall = time.perf_counter() - t_wall
-    barrier(world)
-    ms_per_step = max_over_ranks(world, total / args.steps)
-    value = world * pts * model.nt / (ms_per_step / 1e3) / 1e9
-    # average launch duration of the dominant kernel over the timed region:
-    # the timed per-step time x the stencil's share of a run, the share from
-    # a full run and a stencil-only run timed back to back right after the
-    # timed region (same power / clock state; the share is ~0.99 because the
-    # sparse work rides in the stencil's epilogue)
-    tot2, sten2, _ = op.time(stencil=True)
-    share = min(1.0, sten2 / tot2) if tot2 > 0 else 1.0
-    stencil_launch_ms = ms_per_step / model.nt * share
-    # compulsory bytes: read u(t), u(t-1), m, eta, write u(t+1) = 20 B/pt,
-    # less the eta boxes the kernel skips because they are all zero (the
-    # undamped interior) -- those bytes are not needed, so they are not
-    # counted as achieved bandwidth
-    eta_skip = op.eta_skip_fraction()
+# ---------------------------------------------------------------------------
+# B200 arms
+
+def product_stable_dt(sf):
+    return lambda order, vmax: sf.api._stable_dt(3, order, H, vmax, vmax)
+
+
+def roofline_line(ms_per_step, share, nt, pts, eta_skip, r, traffic):
+    """Dominant kernel (the stencil): algorithmic bytes per launch over its
+    average launch time inside the timed region."""
+    stencil_launch_ms = ms_per_step / nt * share
     alg_bytes = (20 - 4 * eta_skip) * pts
     peak, peak_kind = load_peaks()
     achieved = alg_bytes / (stencil_launch_ms / 1e3) / 1e9
-    traffic = None
+    ops = 21 + 13 * r
+    return ({"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+             "kernel": f"3D stencil (radius {r}) avg launch {stencil_launch_ms * 1e3:.1f} us",
+             "alg_bytes_per_launch": alg_bytes, "eta_boxes_skipped": eta_skip,
+             "frac_of_20B": 20 * pts / (stencil_launch_ms / 1e3) / 1e9 / peak},
+            # second lens for the high orders: the reference's exact fp32
+            # operation count (no FMA contraction) against 148 SMs x 128 lanes
+            {"bound": "fp32", "ops_per_point": ops,
+             "achieved": ops * pts / (stencil_launch_ms / 1e3) / 1e12,
+             "peak": 148 * 128 * 1.965e9 / 1e12, "unit": "Tops/s",
+             "frac": ops * pts / (stencil_launch_ms / 1e3) / (148 * 128 * 1.965e9),
+             "peak_source": "148 SMs x 128 fp32 lanes x 1965 MHz (max SM clock)"})
+
+
+def traffic_of(key):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(args.config)
-        except Exception:
-            traffic = None
+    try:
+        return json.load(open(tpath)).get(key)
+    except Exception:
+        return None
+
+
+def b200_setup(sf, w, device=0, pinned=False, nt=None):
+    """The config's forward operator through the mirrored reference API
+    (acoustic_build), its medium generated on the GPU for smooth configs."""
+    model = sf.AcousticModel(shape=w.shape, boundary_width=w.bw, spacing=w.h,
+                             nt=w.nt if nt is None else nt, dt=w.dt, space_order=w.order,
+                             f0=w.f0, v_top=w.v_top, v_bottom=w.v_bottom,
+                             src_coords=w.src_coords, rec_coords=w.rec_coords)
+    smooth = None
+    if w.smooth is not None:
+        smooth = sf.SmoothMedium(shape=w.shape, seed=w.smooth["seed"], sigma=w.smooth["sigma"],
+                                 v_lo=w.smooth["v_lo"], v_hi=w.smooth["v_hi"],
+                                 boundary_width=w.bw, spacing=w.h, v_min=w.smooth["v_min"])
+    return sf.acoustic_build(model, True, device=device, pinned=pinned, smooth=smooth)
+
+
+def run_b200_arm(args, local):
+    import torch
+
+    import paper_1609_03361_b200 as sf
+    w = workload(args.config, 1, product_stable_dt(sf))
+    setup = b200_setup(sf, w, device=local, pinned=True)
+    op = setup.op
+    pts = interior_points(w.shape, w.order)
+    r = w.order // 2
+    # resident: upload once, warm up (graph capture + clocks), then time
+    op.upload()
+    for _ in range(args.warmup):
+        op.run(0, w.nt)
+    op.synchronize()
+    torch.cuda.set_device(local)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter()
+        total = 0.0
+        nl = 0
+        for _ in range(args.steps):
+            t, _, nl = op.time(stencil=False)
+            total += t
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    ms_per_step = total / args.steps
+    value = pts * w.nt / (ms_per_step / 1e3) / 1e9
+    # the stencil's share of a run: a full run and a stencil-only run timed
+    # back to back right after the timed region (same power / clock state)
+    tot2, sten2, _ = op.time(stencil=True)
+    share = min(1.0, sten2 / tot2) if tot2 > 0 else 1.0
+    roof, comp = roofline_line(ms_per_step, share, w.nt, pts, op.eta_skip_fraction(), r,
+                               traffic_of(args.config))
     # e2e through the C-ABI apply with pinned host buffers
     h2d = sum(a.data.nbytes for a in op.args)
-    # apply returns what the kernel writes: the three slots and the receiver traces
     d2h = setup.field.data.nbytes + setup.rec.data.data.nbytes
     op.apply()  # warm
-    barrier(world)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         op.apply()
-    e2e_s = max_over_ranks(world, (time.perf_counter() - t0) / args.steps)
-    e2e = world * pts * model.nt / e2e_s / 1e9
-    if rank != 0:
-        return
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    e2e = pts * w.nt / e2e_s / 1e9
+    del setup, op
     base = None
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline:
         try:
-            base = cpu_reference_sample(model, args.config, v, vmin, steps=1, warmup=1,
-                                        budget_s=args.cpu_budget)
+            base = ref_acoustic_sample(w, args.cpu_budget, 3, 1)
         except Exception as e:  # reported, not fatal
             base = {"error": str(e)}
     line = {
         "metric": "GPts/s (grid-point updates/sec)", "value": value, "unit": "GPts/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": config_block(args, model),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "peak_source": peak_kind,
-                     "kernel": f"3D stencil (radius {r}) avg launch {stencil_launch_ms * 1e3:.1f} us",
-                     "alg_bytes_per_launch": alg_bytes, "eta_boxes_skipped": eta_skip},
-        # second lens for the high orders: the reference's exact fp32 operation
-        # count (no FMA contraction: 17 + 13r mul/add with c_j*temp3 shared
-        # across the 6 neighbours of one offset, + 4 for the correctly rounded
-        # reciprocal) against the non-FMA fp32 rate, 148 SMs x 128 lanes x clock
-        "compute_roofline": {
-            "bound": "fp32", "ops_per_point": 21 + 13 * r,
-            "achieved": (21 + 13 * r) * pts / (stencil_launch_ms / 1e3) / 1e12,
-            "peak": 148 * 128 * 1.965e9 / 1e12, "unit": "Tops/s",
-            "frac": (21 + 13 * r) * pts / (stencil_launch_ms / 1e3) / (148 * 128 * 1.965e9),
-            "peak_source": "148 SMs x 128 fp32 lanes x 1965 MHz (max SM clock)"},
-        "stencil_share": share,
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "ms_per_time_step": ms_per_step / w.nt,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": config_block(w, "single GPU"),
+        "roofline": roof, "compute_roofline": comp, "stencil_share": share,
         "cpu_baseline": base,
         "e2e": {"value": e2e, "unit": "GPts/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "gpu_launches": int(launches_per_run * args.steps),
-        "clocks": clocks.summary(),
+        "gpu_launches": int(nl * args.steps), "clocks": clocks.summary(),
         "wall_s_timed_region": t_wall,
     }
     print(json.dumps(line), flush=True)
 
 
-def run_b200_diffusion(args, world, rank, local):
+def run_b200_diffusion(args, local):
     """C1: 2048^2 diffusion, alpha 1/2, dx 1/2047, dt = dx^2/4 (weights exactly
     1/4), 500 steps, seeded U[0,1) interior. 2 x 16 MiB slots: L2-resident."""
     from fractions import Fraction
@@ -493,28 +569,30 @@ def run_b200_diffusion(args, world, rank, local):
     op.apply()
     # each apply uploads the pinned host slots, runs all nt steps and reads
     # both slots back in place; consecutive applies continue the run (the
-    # work per apply is identical), so no host-side reset sits in the timed
-    # region (re-filling 32 MiB of host memory per apply took ~3 ms)
+    # work per apply is identical)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         op.apply()
     e2e_s = (time.perf_counter() - t0) / args.steps
     base = None
     if not args.no_cpu_baseline:
-        base = cpu_diffusion_sample(n, nt, args.cpu_budget)
+        base = ref_diffusion_sample(n, nt, args.cpu_budget, 3, 1)
+    l2 = traffic_of("c1")
     line = {
         "metric": "GPts/s (grid-point updates/sec)", "value": value, "unit": "GPts/s",
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "ms_per_time_step": ms / nt,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": diffusion_config_block(c),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                     "frac": achieved / peak, "traffic": l2, "peak_source": peak_kind,
                      "kernel": f"diffusion_tb_kernel (temporal blocking, T=8 steps per "
                                f"launch), {launch_ms * 1e3:.2f} us per time step",
                      "alg_bytes_per_launch": 8 * pts,
                      "note": "achieved = 8 B/pt per time step over the time per step; the "
-                             "field is L2-resident, so HBM does not bind"},
+                             "field is L2-resident, so HBM does not bind (profiles/ "
+                             "r2_c1_l2.txt has the L2 / shared-memory lens)"},
         "cpu_baseline": base,
         "e2e": {"value": pts * nt / e2e_s / 1e9, "unit": "GPts/s",
                 "h2d_bytes_per_step": b.u.data.nbytes, "d2h_bytes_per_step": b.u.data.nbytes},
@@ -523,59 +601,26 @@ def run_b200_diffusion(args, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
-def cpu_diffusion_sample(n, nt, budget_s):
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import oracle_lib as ol
-    rng = np.random.default_rng(2016)
-    u0 = np.zeros((n, n), np.float32)
-    u0[1:-1, 1:-1] = rng.random((n - 2, n - 2))
-    if ol.have_ref():
-        ref = ol.Ref()
-        ref.set_threads(ref.max_threads())
-        def timed(k):
-            op = ol.ref_diffusion(ref, n, n, (1, 2), (1, n - 1), k, 2)
-            op.set("u", np.stack([u0, u0]))
-            op.build()
-            t = time.perf_counter()
-            op.apply()
-            return time.perf_counter() - t
-        cal = timed(10)
-        k = int(max(10, min(nt, budget_s / max(cal / 10, 1e-6))))
-        secs = timed(k)
-        kind, cores = "reference", ref.max_threads()
-    else:
-        port = ol.Port()
-        import multiprocessing
-        k = 20
-        u = np.stack([u0, u0])
-        t = time.perf_counter()
-        port.diffusion_run(u, 2, (1, 2), (1, n - 1), k)
-        secs = time.perf_counter() - t
-        kind, cores = "port", multiprocessing.cpu_count()
-    return {"value": (n - 2) ** 2 * k / secs / 1e9, "unit": "GPts/s", "cores": cores,
-            "kind": kind, "sample": f"c1 {n}^2 diffusion, {k} of {nt} steps, JIT excluded"}
-
-
-def run_b200_fwi(args, world, rank, local):
+def run_b200_fwi(args, local):
     """C5: forward with the full wavefield history in HBM (nt+2 levels of
     301^3), adjoint injecting seeded N(0,1) residuals at 201 x 201 surface
     receivers, gradient accumulated in the adjoint stencil. The metric counts
     the updates of both passes."""
     import paper_1609_03361_b200 as sf
     c = CONFIGS[args.config]
-    shape, order, nt, bw, h = c["shape"], c["order"], c["nt"], c["boundary"], c["spacing"]
+    shape, order, nt = tuple(c["shape"]), c["order"], c["nt"]
     r = order // 2
-    v = smooth_velocity(shape, 1234)
-    g = sf.Grid()
-    model = sf.AcousticModel(shape=shape, boundary_width=bw, spacing=h, nt=nt,
-                             space_order=order, v_top=4500.0, v_bottom=4500.0)
-    dt = min(0.4 * h / 4500.0, model.stable_dt())
-    m, eta = sf.build_medium(g, model, v_field=v, v_min=1500.0)
+    dt = min(0.4 * H / 4500.0, sf.api._stable_dt(3, order, H, 4500.0, 4500.0))
+    sm = sf.SmoothMedium(shape=shape, boundary_width=BW, spacing=H, **{
+        k: v for k, v in SMOOTH.items()})
+    lo, hi = sm.extrema(device=local)
+    m, eta = sm.generate(lo, hi, device=local)
     mid = shape[1] // 2
-    src_c = [[(bw + 2) * h, mid * h, mid * h]]
-    rec_c = [[(bw + 10) * h, (bw + i) * h, (bw + j) * h] for i in range(201) for j in range(201)]
+    src_c = [[(BW + 2) * H, mid * H, mid * H]]
+    rec_c = [[(BW + 10) * H, (BW + i) * H, (BW + j) * H] for i in range(201) for j in range(201)]
+
     def interp(coords):
-        cis, ws = zip(*[sf.interpolation_weights(cc, h, shape) for cc in coords])
+        cis, ws = zip(*[sf.interpolation_weights(cc, H, shape) for cc in coords])
         return np.array(cis, np.int32), np.array(ws, np.float32)
     src_ci, src_w = interp(src_c)
     rec_ci, rec_w = interp(rec_c)
@@ -583,12 +628,11 @@ def run_b200_fwi(args, world, rank, local):
     src = np.array([sf.ricker_wavelet(10.0, t * dt, t0) for t in range(nt)], np.float32)[:, None]
     rng = np.random.default_rng(5)
     residual = rng.standard_normal((nt, len(rec_c)), dtype=np.float32)
-    plan = sf.FwiPlan(shape, order, nt, dt, h, 1, len(rec_c), device=local)
+    plan = sf.FwiPlan(shape, order, nt, dt, H, 1, len(rec_c), device=local)
     # warm-up call (graph capture, sparse index build), then the timed one
-    plan.gradient(m.data, eta.data, src, src_ci, src_w, rec_ci, rec_w, residual)
+    plan.gradient(m, eta, src, src_ci, src_w, rec_ci, rec_w, residual)
     t_e = time.perf_counter()
-    rec_out, grad, _, _ = plan.gradient(m.data, eta.data, src, src_ci, src_w, rec_ci, rec_w,
-                                        residual)
+    rec_out, grad, _, _ = plan.gradient(m, eta, src, src_ci, src_w, rec_ci, rec_w, residual)
     e2e_s = time.perf_counter() - t_e
     fwd = adj = 0.0
     with ClockSampler(local) as clocks:
@@ -598,15 +642,21 @@ def run_b200_fwi(args, world, rank, local):
             adj += a
     fwd /= args.steps
     adj /= args.steps
-    pts = 1
-    for e in shape:
-        pts *= e - 2 * r
+    pts = interior_points(shape, order)
     value = 2 * pts * nt / ((fwd + adj) / 1e3) / 1e9
     peak, peak_kind = load_peaks()
-    # the all-zero eta boxes both sweeps skip (the forward tiling's fraction,
-    # applied to both) are not counted as achieved bytes
     skip = plan.eta_skip_fraction()
     bf, ba = 20 - 4 * skip, 36 - 4 * skip
+    base = None
+    if not args.no_cpu_baseline:
+        try:
+            w = SimpleNamespace(name="c5", block=shape, shape=shape, order=order, nt=nt, bw=BW,
+                                h=H, f0=10.0, dt=dt, v_top=4500.0, v_bottom=4500.0,
+                                smooth=dict(SMOOTH, shape=shape), src_coords=src_c,
+                                rec_coords=rec_c)
+            base = ref_acoustic_sample(w, args.cpu_budget, 3, 1, forward_adjoint=True)
+        except Exception as e:
+            base = {"error": str(e)}
     line = {
         "metric": "GPts/s (grid-point updates/sec)", "value": value, "unit": "GPts/s",
         "n_gpus": 1, "steps": args.steps, "warmup": 1, "ms_per_step": fwd + adj,
@@ -621,9 +671,10 @@ def run_b200_fwi(args, world, rank, local):
                      "adjoint_achieved": ba * pts * nt / (adj / 1e3) / 1e9,
                      "achieved": (bf + ba) * pts * nt / ((fwd + adj) / 1e3) / 1e9,
                      "frac": (bf + ba) * pts * nt / ((fwd + adj) / 1e3) / 1e9 / peak,
-                     "traffic": None, "eta_boxes_skipped": skip},
+                     "traffic": traffic_of("c5"), "eta_boxes_skipped": skip},
+        "cpu_baseline": base,
         "e2e": {"value": 2 * pts * nt / e2e_s / 1e9, "unit": "GPts/s",
-                "h2d_bytes_per_step": m.data.nbytes * 2 + residual.nbytes + src.nbytes,
+                "h2d_bytes_per_step": m.nbytes * 2 + residual.nbytes + src.nbytes,
                 "d2h_bytes_per_step": grad.nbytes + rec_out.nbytes},
         "clocks": clocks.summary(),
     }
@@ -631,10 +682,12 @@ def run_b200_fwi(args, world, rank, local):
 
 
 def run_b200_slabs(args, world, rank, local):
-    """N > 1: weak scaling over depth slabs. The global grid stacks one c2-sized
-    block per GPU along axis 0 ((281 N) x 281 x 281, same boundary, source and
-    receiver line at the top); rank g owns 281 planes and swaps r-deep halos
-    with its neighbours over NCCL inside every time step (sf_plan_attach_nccl)."""
+    """N > 1 (or --force-slabs): weak scaling over depth slabs. The global grid
+    stacks one config block per GPU along axis 0; rank g owns one block's
+    planes and swaps r-deep halos with its neighbours over NCCL inside every
+    time step (sf_plan_attach_nccl). Smooth media are generated per slab on
+    the rank's GPU from global indices, with the global extrema reduced over
+    ranks; no rank ever holds the global medium."""
     import ctypes as C
 
     import torch
@@ -643,39 +696,45 @@ def run_b200_slabs(args, world, rank, local):
     import paper_1609_03361_b200 as sf
     from paper_1609_03361_b200 import _lib
     from paper_1609_03361_b200.slab import SlabPartition, SlabRun, nccl_unique_id
-    base, _, _ = make_model(args.config)
-    if CONFIGS[args.config]["random"]:
-        raise SystemExit("multi-GPU bench uses the c2 layered workload")
-    r = base.space_order // 2
-    gshape = (base.shape[0] * world,) + tuple(base.shape[1:])
-    model = sf.AcousticModel(shape=gshape, boundary_width=base.boundary_width,
-                             spacing=base.spacing, nt=base.nt, dt=base.dt,
-                             space_order=base.space_order, f0=base.f0, v_top=base.v_top,
-                             v_bottom=base.v_bottom, src_coords=base.src_coords,
-                             rec_coords=base.rec_coords)
-    g = sf.Grid()
-    m, eta = sf.build_medium(g, model)
-    src_ci = np.array([sf.interpolation_weights(c, model.spacing, gshape)[0]
-                       for c in model.src_coords], np.int32)
-    src_w = np.array([sf.interpolation_weights(c, model.spacing, gshape)[1]
-                      for c in model.src_coords], np.float32)
-    rec_ci = np.array([sf.interpolation_weights(c, model.spacing, gshape)[0]
-                       for c in model.rec_coords], np.int32)
-    rec_w = np.array([sf.interpolation_weights(c, model.spacing, gshape)[1]
-                      for c in model.rec_coords], np.float32)
-    t0 = 1.0 / model.f0
-    ser = np.array([sf.ricker_wavelet(model.f0, t * model.dt, t0) for t in range(model.nt)],
-                   np.float32)[:, None]
-    rec = np.zeros((model.nt, len(rec_ci)), np.float32)
+    w = workload(args.config, world, product_stable_dt(sf))
+    gshape = w.shape
+    r = w.order // 2
     part = SlabPartition.split(gshape[0], r, world, rank)
-    slab = SlabRun(part, gshape, model.space_order, True, model.nt, model.dt, model.spacing,
-                   m.data, eta.data, ser, src_ci, src_w, rec, rec_ci, rec_w, device=local)
+    lshape = (part.local_n0,) + tuple(gshape[1:])
+    if w.smooth is None:
+        model = sf.AcousticModel(shape=gshape, boundary_width=w.bw, spacing=w.h, nt=w.nt,
+                                 dt=w.dt, space_order=w.order, f0=w.f0, v_top=w.v_top,
+                                 v_bottom=w.v_bottom)
+        m, eta = sf.build_medium(sf.Grid(), model)
+        m_loc = np.ascontiguousarray(m.data[part.local()])
+        eta_loc = np.ascontiguousarray(eta.data[part.local()])
+    else:
+        sm = sf.SmoothMedium(shape=gshape, seed=w.smooth["seed"], sigma=w.smooth["sigma"],
+                             v_lo=w.smooth["v_lo"], v_hi=w.smooth["v_hi"], boundary_width=w.bw,
+                             spacing=w.h, v_min=w.smooth["v_min"])
+        lo, hi = sm.extrema(part.own_begin, part.own_end, device=local)
+        lo = reduce_over_ranks(world, lo, "min")
+        hi = reduce_over_ranks(world, hi, "max")
+        m_loc, eta_loc = sm.generate(lo, hi, part.plane0, part.plane_end, device=local)
+
+    def interp(coords):
+        cis, ws = zip(*[sf.interpolation_weights(cc, w.h, gshape) for cc in coords])
+        return np.array(cis, np.int32), np.array(ws, np.float32)
+    src_ci, src_w = interp(w.src_coords)
+    rec_ci, rec_w = interp(w.rec_coords)
+    t0 = 1.0 / w.f0
+    ser = np.array([sf.ricker_wavelet(w.f0, t * w.dt, t0) for t in range(w.nt)],
+                   np.float32)[:, None].repeat(len(src_ci), axis=1)
+    rec = np.zeros((w.nt, len(rec_ci)), np.float32)
+    slab = SlabRun(part, gshape, w.order, True, w.nt, w.dt, w.h, m_loc, eta_loc, ser, src_ci,
+                   src_w, rec, rec_ci, rec_w, device=local, local_medium=True)
+    del m_loc, eta_loc
     obj = [nccl_unique_id() if rank == 0 else None]
     if world > 1:
         dist.broadcast_object_list(obj, src=0)
     slab.attach_nccl(obj[0], world, rank)
     for _ in range(args.warmup):
-        slab.run(0, model.nt)
+        slab.run(0, w.nt)
     barrier(world)
     tot = C.c_float()
     sten = C.c_float()
@@ -686,16 +745,19 @@ def run_b200_slabs(args, world, rank, local):
             sf.api.check(_lib.lib.sf_plan_time(slab.plan, C.byref(tot), None, C.byref(nl)))
             total += tot.value
     barrier(world)
-    ms_per_step = max_over_ranks(world, total / args.steps)
+    ms_per_step = reduce_over_ranks(world, total / args.steps)
     # per-rank stencil-only pass (no exchange) for the roofline of the kernel
     sf.api.check(_lib.lib.sf_plan_time(slab.plan, C.byref(tot), C.byref(sten), C.byref(nl)))
-    sten_ms = max_over_ranks(world, sten.value)
-    pts = 1
-    for e in gshape:
-        pts *= e - 2 * r
-    value = pts * model.nt / (ms_per_step / 1e3) / 1e9
+    share = reduce_over_ranks(world, min(1.0, sten.value / tot.value) if tot.value > 0 else 1.0)
+    pts = interior_points(gshape, w.order)
+    value = pts * w.nt / (ms_per_step / 1e3) / 1e9
+    frac = C.c_double()
+    sf.api.check(_lib.lib.sf_plan_eta_skip_fraction(slab.plan, C.byref(frac)))
+    own_pts = interior_points(w.block, w.order)  # a rank's share of the interior
+    roof, comp = roofline_line(ms_per_step, share, w.nt, own_pts, frac.value, r, None)
     # e2e: upload host slices, run, download, every step (pinned host buffers,
     # as in the single-GPU arm)
+
     def pinned(a):
         t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
         arr = t.numpy()
@@ -708,39 +770,32 @@ def run_b200_slabs(args, world, rank, local):
     for _ in range(args.steps):
         argv = (C.c_void_p * 9)(*[b.ctypes.data for b in slab.bufs])
         sf.api.check(_lib.lib.sf_plan_invoke(slab.plan, argv, 9))
-    e2e_s = max_over_ranks(world, (time.perf_counter() - t_e) / args.steps)
-    h2d = sum(b.nbytes for b in slab.bufs)
-    d2h = slab.bufs[0].nbytes + slab.bufs[6].nbytes
+    e2e_s = reduce_over_ranks(world, (time.perf_counter() - t_e) / args.steps)
+    h2d = reduce_over_ranks(world, float(sum(b.nbytes for b in slab.bufs))) * world
+    d2h = reduce_over_ranks(world, float(slab.bufs[0].nbytes + slab.bufs[6].nbytes)) * world
+    base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            base = ref_acoustic_sample(w, args.cpu_budget, 3, 1)
+        except Exception as e:
+            base = {"error": str(e)}
     if rank == 0:
+        cfg = config_block(w, f"slab{world}")
+        cfg["workload"] += (f"; {world} depth slab(s) of {w.block[0]} planes, NCCL halo "
+                            f"exchange ({r} planes per face) every step")
+        cfg["local_grid"] = list(lshape)
         line = {
             "metric": "GPts/s (grid-point updates/sec)", "value": value, "unit": "GPts/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config} stacked along depth: "
-                                   f"{'x'.join(map(str, gshape))}, order {model.space_order}, "
-                                   f"{model.nt} steps, {world} depth slabs of "
-                                   f"{base.shape[0]} planes, NCCL halo exchange ({r} planes) "
-                                   "every step", "grid": list(gshape),
-                       "parallelism": f"slab{world}", "interior_points": pts},
-            "e2e": {"value": pts * model.nt / e2e_s / 1e9, "unit": "GPts/s",
-                    "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world},
+            "ms_per_step": ms_per_step, "ms_per_time_step": ms_per_step / w.nt,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": cfg, "roofline": roof, "compute_roofline": comp,
+            "stencil_share": share, "cpu_baseline": base,
+            "e2e": {"value": pts * w.nt / e2e_s / 1e9, "unit": "GPts/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(nl.value * args.steps),
             "clocks": clocks.summary(),
         }
-        peak, peak_kind = load_peaks()
-        own_pts = pts // world  # each rank updates its own slab's interior share
-        import ctypes
-        frac = ctypes.c_double()
-        sf.api.check(_lib.lib.sf_plan_eta_skip_fraction(slab.plan, ctypes.byref(frac)))
-        bpp = 20 - 4 * frac.value  # less the all-zero eta boxes the kernel skips
-        achieved = bpp * own_pts / (sten_ms / model.nt / 1e3) / 1e9
-        line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                            "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
-                            "kernel": f"3D stencil (radius {r}) per rank, avg launch "
-                                      f"{sten_ms / model.nt * 1e3:.1f} us (stencil-only pass)",
-                            "alg_bytes_per_launch": bpp * own_pts,
-                            "eta_boxes_skipped": frac.value}
         print(json.dumps(line), flush=True)
     slab.close()
 
@@ -751,28 +806,35 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-budget", type=float, default=20.0,
+                    help="seconds of CPU work for the product line's cpu_baseline sample")
+    ap.add_argument("--ref-budget", type=float, default=60.0,
+                    help="seconds of CPU work for the reference arm's timed applies")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     # exercise the multi-GPU slab path (NCCL communicator, slab plans) with a
     # single rank: validates the N > 1 code on a one-GPU box
     ap.add_argument("--force-slabs", action="store_true")
     args = ap.parse_args()
-    world, rank, local = dist_init(args)
+    world, rank, local = dist_init()
+    kind = CONFIGS[args.config].get("kind", "acoustic")
+    if args.impl == "reference":
+        # rank 0 alone runs the CPU reference; the others exit without work
+        run_reference_arm(args, world, rank)
+        return
+    if world > 1:
+        dist_start(local)
     try:
-        kind = CONFIGS[args.config].get("kind", "acoustic")
-        if args.impl == "reference":
-            run_reference_arm(args, world, rank)
-        elif kind == "diffusion":
+        if kind == "diffusion":
             if rank == 0:
-                run_b200_diffusion(args, world, rank, local)
+                run_b200_diffusion(args, local)
         elif kind == "fwi":
             if rank == 0:
-                run_b200_fwi(args, world, rank, local)
+                run_b200_fwi(args, local)
         elif world > 1 or args.force_slabs:
             run_b200_slabs(args, world, rank, local)
         else:
-            run_b200_arm(args, world, rank, local)
+            run_b200_arm(args, local)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -159,6 +159,37 @@ double sf_ricker(double f0, double t, double t0);
 int sf_build_medium(int ndim, const int64_t *shape, int boundary_width,
                     double spacing, double v_top, double v_bottom,
                     const double *v_field, double v_min, float *m, float *eta);
+/* ---- seeded smooth random media (configs C3/C4/C5) ---------
+ * Velocity = seeded hash noise filtered by a separable Gaussian (sigma cells,
+ * radius int(4 sigma + 0.5), mirrored at the faces), rescaled to
+ * [v_lo, v_hi] with the extrema of the GLOBAL grid; m / eta then follow
+ * build_medium (acoustic.cpp:67-105) per cell, from global indices. Every
+ * value depends only on its global index, so slabs generate their own planes
+ * (src/medium.cu documents the exact definition; oracle/sf_port.c restates
+ * it for the tests). No reference counterpart: the reference takes media
+ * only as host arrays (GridFunction::set, grid.cpp:103-126).             */
+typedef struct {
+    int64_t shape[3];          /* global extents, axis 0 slowest */
+    int64_t a0_begin, a0_end;  /* global axis-0 planes to generate */
+    uint64_t seed;
+    double sigma;              /* filter width in cells */
+    double v_lo, v_hi;         /* velocity range after the rescale, m/s */
+    int boundary_width;        /* sponge, as build_medium */
+    double spacing;
+    double v_min;              /* sponge strength (build_medium's v_min) */
+} sf_smooth_medium_desc;
+/* Extrema of the filtered noise over planes [a0_begin, a0_end) (slabs: take
+ * the min / max over ranks before generating). */
+int sf_smooth_extrema(const sf_smooth_medium_desc *desc, int device, double *lo, double *hi);
+/* m, eta of planes [a0_begin, a0_end) into dense host arrays. */
+int sf_smooth_medium(const sf_smooth_medium_desc *desc, double lo, double hi, int device,
+                     float *m, float *eta);
+/* Same, straight into a plan's resident m / eta (HBM, no host copy): the
+ * plan's own planes (slab plans: global plane0 .. plane0 + local n0) of the
+ * global grid desc->shape; desc->a0_begin/a0_end are ignored. */
+int sf_plan_set_smooth_medium(sf_plan *plan, const sf_smooth_medium_desc *desc, double lo,
+                              double hi);
+
 /* Folded fp32 stencil constants the plan uses (for inspection/tests):
  * out[0]=ce, [1]=cm, [2..4]=time-term coefficients in emitted order,
  * [5]=centre, [6..6+r)=neighbour j=1..r, [14]=injection scale;

@@ -544,3 +544,184 @@ int sfp_diffusion_run(int64_t nx, int64_t ny, int order, float c0, int has_c0,
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------------
+ * Seeded smooth random medium (configs C3/C4/C5). The product generates it
+ * on the GPU (paper_1609_03361_b200/csrc/medium.cu, which states the
+ * definition); this is the same definition in plain C, evaluated in the
+ * same order (double sums in ascending tap order, no contraction), so the
+ * two agree bitwise. The m / eta expressions are build_medium's
+ * (acoustic.cpp:67-105), with global indices. */
+
+static int64_t sm_reflect(int64_t i, int64_t n) {
+    int64_t p = 2 * n;
+    i %= p;
+    if (i < 0) i += p;
+    return i < n ? i : p - 1 - i;
+}
+
+static uint64_t sm_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static double sm_noise(uint64_t salt, int64_t lin) {
+    uint64_t z = sm_mix((uint64_t)lin * 0x9E3779B97F4A7C15ull + salt);
+    return (double)((int64_t)(z >> 40) - 8388608) * (1.0 / 8388608.0);
+}
+
+int sfp_smooth_taps(double sigma, double *g /* [2*64+1] */) {
+    int rad = (int)(4.0 * sigma + 0.5);
+    if (!(sigma > 0) || rad < 1 || rad > 64) return -1;
+    double sum = 0.0;
+    for (int k = 0; k <= 2 * rad; ++k) {
+        double x = (double)(k - rad);
+        g[k] = exp(-0.5 * x * x / (sigma * sigma));
+        sum += g[k];
+    }
+    for (int k = 0; k <= 2 * rad; ++k) g[k] /= sum;
+    return rad;
+}
+
+/* t2 (axis-2 then axis-1 filtered noise) of the planes the depth pass over
+ * [b, e) reads; *L = global index of its first plane. */
+static float *sm_t2(const int64_t *shape, int64_t b, int64_t e, uint64_t seed,
+                    const double *g, int rad, int64_t *L) {
+    int64_t n0 = shape[0], n1 = shape[1], n2 = shape[2];
+    int64_t lo = n0, hi = 0;
+    for (int64_t p = b - rad; p < e + rad; ++p) {
+        int64_t q = sm_reflect(p, n0);
+        if (q < lo) lo = q;
+        if (q + 1 > hi) hi = q + 1;
+    }
+    *L = lo;
+    int64_t nz = hi - lo, n12 = n1 * n2;
+    float *t2 = (float *)malloc(sizeof(float) * (size_t)(nz * n12));
+    if (!t2) return NULL;
+    uint64_t salt = sm_mix(seed + 0x9E3779B97F4A7C15ull);
+    int64_t *r1 = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n1 + 2 * rad));
+    for (int64_t i = 0; i < n1 + 2 * rad; ++i) r1[i] = sm_reflect(i - rad, n1) * n2;
+#pragma omp parallel
+    {
+        float *t1 = (float *)malloc(sizeof(float) * (size_t)n12);
+        double *row = (double *)malloc(sizeof(double) * (size_t)(n2 + 2 * rad));
+        double *acc = (double *)malloc(sizeof(double) * (size_t)n2);
+#pragma omp for schedule(static)
+        for (int64_t z = 0; z < nz; ++z) {
+            int64_t i0 = lo + z;
+            for (int64_t i1 = 0; i1 < n1; ++i1) {
+                int64_t rowlin = (i0 * n1 + i1) * n2;
+                /* row[j] = noise at a2 = refl(j - rad) */
+                for (int64_t j = 0; j < n2 + 2 * rad; ++j)
+                    row[j] = sm_noise(salt, rowlin + sm_reflect(j - rad, n2));
+                for (int64_t i2 = 0; i2 < n2; ++i2) {
+                    double s = 0.0;
+                    for (int k = 0; k <= 2 * rad; ++k) s = s + g[k] * row[i2 + k];
+                    t1[i1 * n2 + i2] = (float)s;
+                }
+            }
+            float *out = t2 + z * n12;
+            for (int64_t i1 = 0; i1 < n1; ++i1) {
+                for (int64_t i2 = 0; i2 < n2; ++i2) acc[i2] = 0.0;
+                for (int k = 0; k <= 2 * rad; ++k) {
+                    const float *src = t1 + r1[i1 + k];
+                    double gk = g[k];
+                    for (int64_t i2 = 0; i2 < n2; ++i2) acc[i2] = acc[i2] + gk * (double)src[i2];
+                }
+                for (int64_t i2 = 0; i2 < n2; ++i2) out[i1 * n2 + i2] = (float)acc[i2];
+            }
+        }
+        free(t1);
+        free(row);
+        free(acc);
+    }
+    free(r1);
+    return t2;
+}
+
+/* f of global plane i0 (depth pass) into acc[n1*n2] */
+static void sm_depth(const float *t2, int64_t L, const int64_t *shape, int64_t i0,
+                     const double *g, int rad, double *acc) {
+    int64_t n12 = shape[1] * shape[2];
+    for (int64_t j = 0; j < n12; ++j) acc[j] = 0.0;
+    for (int k = 0; k <= 2 * rad; ++k) {
+        const float *src = t2 + (sm_reflect(i0 + k - rad, shape[0]) - L) * n12;
+        double gk = g[k];
+        for (int64_t j = 0; j < n12; ++j) acc[j] = acc[j] + gk * (double)src[j];
+    }
+}
+
+int sfp_smooth_extrema(const int64_t *shape, int64_t b, int64_t e, uint64_t seed,
+                       double sigma, double *lo_out, double *hi_out) {
+    double g[129];
+    int rad = sfp_smooth_taps(sigma, g);
+    if (rad < 0 || b < 0 || e > shape[0] || b >= e) return 1;
+    int64_t L;
+    float *t2 = sm_t2(shape, b, e, seed, g, rad, &L);
+    if (!t2) return 7;
+    int64_t n12 = shape[1] * shape[2];
+    double lo = INFINITY, hi = -INFINITY;
+#pragma omp parallel
+    {
+        double *acc = (double *)malloc(sizeof(double) * (size_t)n12);
+        double l = INFINITY, h = -INFINITY;
+#pragma omp for schedule(static)
+        for (int64_t i0 = b; i0 < e; ++i0) {
+            sm_depth(t2, L, shape, i0, g, rad, acc);
+            for (int64_t j = 0; j < n12; ++j) {
+                if (acc[j] < l) l = acc[j];
+                if (acc[j] > h) h = acc[j];
+            }
+        }
+#pragma omp critical
+        {
+            if (l < lo) lo = l;
+            if (h > hi) hi = h;
+        }
+        free(acc);
+    }
+    free(t2);
+    *lo_out = lo;
+    *hi_out = hi;
+    return 0;
+}
+
+int sfp_smooth_medium(const int64_t *shape, int64_t b, int64_t e, uint64_t seed,
+                      double sigma, double v_lo, double v_hi, int boundary_width,
+                      double spacing, double v_min, double lo, double hi, float *m,
+                      float *eta) {
+    double g[129];
+    int rad = sfp_smooth_taps(sigma, g);
+    if (rad < 0 || b < 0 || e > shape[0] || b >= e || !(hi > lo)) return 1;
+    int64_t L;
+    float *t2 = sm_t2(shape, b, e, seed, g, rad, &L);
+    if (!t2) return 7;
+    int64_t n0 = shape[0], n1 = shape[1], n2 = shape[2], n12 = n1 * n2;
+    const long w = boundary_width;
+    const double sigma_max =
+        1.5 * log(1000.0) * v_min / ((double)(w > 1 ? w : 1) * spacing);
+#pragma omp parallel
+    {
+        double *acc = (double *)malloc(sizeof(double) * (size_t)n12);
+#pragma omp for schedule(static)
+        for (int64_t i0 = b; i0 < e; ++i0) {
+            sm_depth(t2, L, shape, i0, g, rad, acc);
+            for (int64_t i1 = 0; i1 < n1; ++i1)
+                for (int64_t i2 = 0; i2 < n2; ++i2) {
+                    double f = acc[i1 * n2 + i2];
+                    double v = v_lo + ((v_hi - v_lo) * (f - lo)) / (hi - lo);
+                    double mv = 1.0 / (v * v);
+                    int64_t idx[3] = {i0, i1, i2};
+                    double sg = sponge_sigma(3, shape, idx, w, sigma_max);
+                    int64_t off = ((i0 - b) * n1 + i1) * n2 + i2;
+                    m[off] = (float)mv;
+                    eta[off] = (float)(mv * sg);
+                }
+        }
+        free(acc);
+    }
+    (void)n0;
+    free(t2);
+    return 0;
+}

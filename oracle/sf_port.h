@@ -139,6 +139,20 @@ int sfp_diffusion_coefs(sfp_rat alpha, sfp_rat dx, int order, float *c0,
 int sfp_diffusion_run(int64_t nx, int64_t ny, int order, float c0, int has_c0,
                       const float *cj, int64_t nt, float *u, int nthreads);
 
+
+/* Seeded smooth random medium (configs C3/C4/C5): the definition stated in
+ * paper_1609_03361_b200/csrc/medium.cu, restated here. Taps: returns the
+ * filter radius (or -1), g[0..2*rad]. Extrema of the filtered noise over
+ * global planes [b, e); m / eta (dense [e-b][n1][n2]) of those planes from
+ * the global extrema lo / hi. Returns 0 on success. */
+int sfp_smooth_taps(double sigma, double *g /* [129] */);
+int sfp_smooth_extrema(const int64_t *shape, int64_t b, int64_t e, uint64_t seed,
+                       double sigma, double *lo, double *hi);
+int sfp_smooth_medium(const int64_t *shape, int64_t b, int64_t e, uint64_t seed,
+                      double sigma, double v_lo, double v_hi, int boundary_width,
+                      double spacing, double v_min, double lo, double hi, float *m,
+                      float *eta);
+
 #ifdef __cplusplus
 }
 #endif

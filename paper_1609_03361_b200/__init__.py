@@ -11,7 +11,7 @@ from .api import (  # noqa: F401
     AcousticModel, AcousticSetup, AdjointTestResult, CflViolationError, CudaError,
     DiffusionConfig, FwiPlan, Grid, GridFunction, InvalidOrderError, InvalidShapeError,
     KernelFailedError, Operator, OutOfDomainError, SfError, SignatureMismatchError,
-    SparsePointSet, acoustic_adjoint, acoustic_build, acoustic_forward, adjoint_test,
+    SmoothMedium, SparsePointSet, acoustic_adjoint, acoustic_build, acoustic_forward, adjoint_test,
     adjoint_test_with, build_medium, diffusion_run, gaussian_blob_field, hot_cell_field,
     interpolation_weights, load_series_column, make_diffusion_operator, ricker_wavelet,
 )

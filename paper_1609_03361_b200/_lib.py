@@ -40,7 +40,8 @@ EXPORTS = [
     "sf_acoustic_plan_create_slab", "sf_slab_chain_run", "sf_nccl_unique_id",
     "sf_plan_attach_nccl", "sf_plan_autotune", "sf_plan_save_buffer", "sf_plan_load_buffer",
     "sf_plan_dump_csv", "sf_plan_save_series_text", "sf_selftest_reciprocal",
-    "sf_plan_eta_skip_fraction",
+    "sf_plan_eta_skip_fraction", "sf_smooth_extrema", "sf_smooth_medium",
+    "sf_plan_set_smooth_medium",
 ]
 
 
@@ -68,6 +69,13 @@ class TuneEntry(C.Structure):
 class SlabDesc(C.Structure):
     _fields_ = [("global_n0", C.c_int64), ("plane0", C.c_int64), ("own_begin", C.c_int64),
                 ("own_end", C.c_int64)]
+
+
+class SmoothMediumDesc(C.Structure):
+    _fields_ = [("shape", C.c_int64 * 3), ("a0_begin", C.c_int64), ("a0_end", C.c_int64),
+                ("seed", C.c_uint64), ("sigma", C.c_double), ("v_lo", C.c_double),
+                ("v_hi", C.c_double), ("boundary_width", C.c_int), ("spacing", C.c_double),
+                ("v_min", C.c_double)]
 
 
 _vp = C.c_void_p
@@ -129,6 +137,12 @@ def _bind(lib):
     lib.sf_plan_eta_skip_fraction.argtypes = [_vp, C.POINTER(C.c_double)]
     lib.sf_plan_autotune.argtypes = [_vp, C.c_int64, C.c_int, C.POINTER(TuneEntry), C.c_int,
                                      C.POINTER(C.c_int)]
+    lib.sf_smooth_extrema.argtypes = [C.POINTER(SmoothMediumDesc), C.c_int,
+                                      C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    lib.sf_smooth_medium.argtypes = [C.POINTER(SmoothMediumDesc), C.c_double, C.c_double,
+                                     C.c_int, _vp, _vp]
+    lib.sf_plan_set_smooth_medium.argtypes = [_vp, C.POINTER(SmoothMediumDesc), C.c_double,
+                                              C.c_double]
     return lib
 
 

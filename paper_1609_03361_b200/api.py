@@ -423,10 +423,18 @@ class AcousticSetup:
     dt: float
 
 
-def build_medium(grid: Grid, model: AcousticModel, v_field=None, v_min=None):
-    """m and eta (acoustic.cpp:67-105); v_field overrides the two layers."""
+def build_medium(grid: Grid, model: AcousticModel, v_field=None, v_min=None, smooth=None,
+                 device=0):
+    """m and eta (acoustic.cpp:67-105); v_field overrides the two layers,
+    `smooth` (a SmoothMedium of the model's shape) generates them on the GPU."""
     m = grid.create_dense("m", model.shape, model.space_order)
     eta = grid.create_dense("eta", model.shape, model.space_order)
+    if smooth is not None:
+        if tuple(smooth.shape) != tuple(model.shape):
+            raise InvalidShapeError("smooth medium shape differs from the model")
+        lo, hi = smooth.extrema(device=device)
+        smooth.generate(lo, hi, device=device, out=(m.data, eta.data))
+        return m, eta
     shape = np.asarray(model.shape, np.int64)
     vptr = None
     if v_field is not None:
@@ -438,6 +446,53 @@ def build_medium(grid: Grid, model: AcousticModel, v_field=None, v_min=None):
                               float(v_min if v_min is not None else 0.0),
                               m.data.reshape(-1), eta.data.reshape(-1)))
     return m, eta
+
+
+@dataclass
+class SmoothMedium:
+    """Seeded smooth random medium (configs C3/C4/C5): Gaussian-
+    filtered hash noise rescaled to [v_lo, v_hi], then build_medium's m / eta
+    (acoustic.cpp:67-105). Generated on the GPU from global indices
+    (csrc/medium.cu), so a depth slab makes only its own planes; the global
+    extrema come from `extrema()` over every slab (min / max over ranks)."""
+    shape: tuple
+    seed: int = 1234
+    sigma: float = 8.0
+    v_lo: float = 1500.0
+    v_hi: float = 4500.0
+    boundary_width: int = 40
+    spacing: float = 10.0
+    v_min: float = 1500.0
+
+    def desc(self, a0_begin=0, a0_end=None):
+        d = _lib.SmoothMediumDesc()
+        for i, e in enumerate(self.shape):
+            d.shape[i] = e
+        d.a0_begin = a0_begin
+        d.a0_end = self.shape[0] if a0_end is None else a0_end
+        d.seed, d.sigma, d.v_lo, d.v_hi = self.seed, self.sigma, self.v_lo, self.v_hi
+        d.boundary_width, d.spacing, d.v_min = self.boundary_width, self.spacing, self.v_min
+        return d
+
+    def extrema(self, a0_begin=0, a0_end=None, device=0):
+        lo, hi = C.c_double(), C.c_double()
+        check(lib.sf_smooth_extrema(C.byref(self.desc(a0_begin, a0_end)), device, C.byref(lo),
+                                    C.byref(hi)))
+        return lo.value, hi.value
+
+    def generate(self, lo, hi, a0_begin=0, a0_end=None, device=0, out=None):
+        """m, eta of global planes [a0_begin, a0_end) as dense host arrays."""
+        e = self.shape[0] if a0_end is None else a0_end
+        shp = (e - a0_begin,) + tuple(self.shape[1:])
+        m, eta = out if out is not None else (np.empty(shp, np.float32), np.empty(shp, np.float32))
+        assert m.shape == shp and eta.shape == shp and m.flags.c_contiguous
+        check(lib.sf_smooth_medium(C.byref(self.desc(a0_begin, e)), lo, hi, device,
+                                   m.ctypes.data, eta.ctypes.data))
+        return m, eta
+
+    def set_plan(self, op: "Operator", lo, hi):
+        """Write m / eta straight into a plan's HBM mirrors (its own planes)."""
+        check(lib.sf_plan_set_smooth_medium(op._plan, C.byref(self.desc()), lo, hi))
 
 
 def _fill_series(pts: SparsePointSet, series, model: AcousticModel):
@@ -455,7 +510,8 @@ def _fill_series(pts: SparsePointSet, series, model: AcousticModel):
 
 
 def acoustic_build(model: AcousticModel, forward_run: bool, src_series=None, rec_series=None,
-                   device=0, v_field=None, v_min=None, pinned=False) -> AcousticSetup:
+                   device=0, v_field=None, v_min=None, pinned=False,
+                   smooth=None) -> AcousticSetup:
     """Configure without executing (acoustic.cpp:128-206)."""
     if model.dims() < 2 or model.dims() > 3:
         raise InvalidShapeError("acoustic model needs 2 or 3 dimensions")
@@ -465,7 +521,7 @@ def acoustic_build(model: AcousticModel, forward_run: bool, src_series=None, rec
     grid = Grid(pinned=pinned)
     fname = "u" if forward_run else "v"
     fld = grid.create_time(fname, model.shape, 2, model.space_order)
-    m, eta = build_medium(grid, model, v_field, v_min)
+    m, eta = build_medium(grid, model, v_field, v_min, smooth, device)
     src_coords = model.src_coords or model.default_src()
     rec_coords = model.rec_coords or model.default_rec()
     src = SparsePointSet(grid, "src", src_coords, model.nt, model.spacing, fld)
@@ -693,6 +749,16 @@ class FwiPlan:
         i32 = lambda a: np.ascontiguousarray(a, np.int32)  # noqa: E731
         ins = [f32(m), f32(eta), f32(src), i32(src_ci), f32(src_w), i32(rec_ci), f32(rec_w),
                f32(residual)]
+        # the C side reads the plan's full extents from every buffer: check
+        # sizes here (InvalidShapeError, as Operator._argv does)
+        want = [("m", self.shape), ("eta", self.shape), ("src", (self.nt, self.n_src)),
+                ("src_ci", (self.n_src, 3)), ("src_w", (self.n_src, 8)),
+                ("rec_ci", (self.n_rec, 3)), ("rec_w", (self.n_rec, 8)),
+                ("residual", (self.nt, self.n_rec))]
+        for a, (name, shp) in zip(ins, want):
+            if a.size != int(np.prod(shp)):
+                raise InvalidShapeError(f"{name} must have {int(np.prod(shp))} elements "
+                                        f"{shp}, got {a.size}")
         rec_out = np.zeros((self.nt, self.n_rec), np.float32)
         grad = np.zeros(self.shape, np.float32)
         v = np.zeros((3,) + self.shape, np.float32) if want_v else None

@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <numeric>
@@ -45,6 +46,7 @@
 #include "vec_stencil.cuh"
 #include "diffusion_tb.cuh"
 #include "sf_internal.h"
+#include "medium.h"
 
 namespace sfb {
 
@@ -2281,7 +2283,15 @@ extern "C" int sf_plan_autotune(sf_plan* p, int64_t tune_steps, int repeats, sf_
         const size_t fbytes = sizeof(float) * (p->slot_elems + field_slack(*p));
         const size_t sbytes = sizeof(float) * p->nt * p->src.np;
         const size_t rbytes = sizeof(float) * p->nt * p->rec.np;
-        std::vector<float*> snap;
+        // snapshot buffers freed, and the plan put back on its original
+        // configuration with its state restored, on every exit path
+        struct Snap {
+            std::vector<float*> bufs;
+            ~Snap() {
+                for (float* f : bufs) dfree(f);
+            }
+        } snap_guard;
+        std::vector<float*>& snap = snap_guard.bufs;
         auto copy = [&](void* dst, const void* src, size_t n) {
             SF_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, p->stream));
         };
@@ -2299,6 +2309,25 @@ extern "C" int sf_plan_autotune(sf_plan* p, int64_t tune_steps, int repeats, sf_
         StencilConfig best = original;
         float best_ms = -1.0f;
         int n = 0;
+        struct Revert {
+            sf_plan* p;
+            const StencilConfig& cfg;
+            std::function<void(bool)>& restore;
+            bool armed = true;
+            ~Revert() {
+                if (!armed) return;
+                try {
+                    cudaStreamSynchronize(p->stream);
+                    clear_graphs(*p);
+                    apply_config(*p, cfg);
+                    restore(false);
+                    cudaStreamSynchronize(p->stream);
+                } catch (...) {
+                }
+            }
+        };
+        std::function<void(bool)> restore_fn = restore;
+        Revert revert{p, original, restore_fn};
         for (const StencilConfig& c : tune_candidates(*p)) {
             try {
                 apply_config(*p, c);
@@ -2331,7 +2360,7 @@ extern "C" int sf_plan_autotune(sf_plan* p, int64_t tune_steps, int repeats, sf_
         apply_config(*p, best);
         restore(false);
         SF_CUDA(cudaStreamSynchronize(p->stream));
-        for (float* f : snap) dfree(f);
+        revert.armed = false;
         if (n_entries) *n_entries = n;
     });
 }
@@ -2573,6 +2602,23 @@ extern "C" int sf_selftest_reciprocal(int device, unsigned long long* mismatches
     });
 }
 
+namespace sfb {
+namespace {
+// medium.cu reports MediumError; map it onto the status codes
+template <typename F>
+int medium_guard(F&& f) {
+    return guard([&] {
+        try {
+            f();
+        } catch (const sfb::MediumError& e) {
+            throw sfb::Status(e.code == 1 ? SF_ERR_OOM : e.code == 2 ? SF_ERR_CUDA : SF_ERR_INVALID,
+                              e.what());
+        }
+    });
+}
+}  // namespace
+}  // namespace sfb
+
 extern "C" {
 
 const char* sf_last_error(void) { return sfb::g_error.c_str(); }
@@ -2744,6 +2790,10 @@ int sf_slab_chain_run(sf_plan* const* plans, int nplans, int64_t b, int64_t e) {
         for (int i = 0; i < nplans; ++i) {  // all-zero eta boxes of each slab (its own planes)
             SF_CUDA(cudaSetDevice(plans[i]->device));
             sfb::ensure_eta_flags(*plans[i]);
+            // the stencil's TMA producer reads the flag words before its
+            // griddepcontrol.wait: the first (PDL) launch of the chain must not
+            // overlap the flags kernel, so finish it here
+            SF_CUDA(cudaStreamSynchronize(plans[i]->stream));
         }
         for (int64_t k = b; k < e; ++k) sfb::chain_step(plans, nplans, k);
         for (int i = 0; i < nplans; ++i) sfb::check_kernel_errors(*plans[i]);
@@ -2988,6 +3038,51 @@ int sf_build_medium(int ndim, const int64_t* shape, int boundary_width, double s
     sfb::build_medium(ndim, shape, boundary_width, spacing, v_top, v_bottom, v_field, v_min, m,
                       eta);
     return SF_OK;
+}
+
+
+int sf_smooth_extrema(const sf_smooth_medium_desc* d, int device, double* lo, double* hi) {
+    if (!d || !lo || !hi) return SF_ERR_INVALID;
+    return sfb::medium_guard([&] {
+        SF_CUDA(cudaSetDevice(device));
+        sfb::smooth_medium_run(*d, 0, lo, hi, nullptr, nullptr, 0, 0, nullptr);
+    });
+}
+
+int sf_smooth_medium(const sf_smooth_medium_desc* d, double lo, double hi, int device, float* m,
+                     float* eta) {
+    if (!d || !m || !eta) return SF_ERR_INVALID;
+    return sfb::medium_guard([&] {
+        SF_CUDA(cudaSetDevice(device));
+        if (d->shape[0] < 1 || d->shape[1] < 1 || d->shape[2] < 1 || d->a0_end <= d->a0_begin)
+            throw sfb::Status(SF_ERR_INVALID, "smooth medium: empty range");
+        const int64_t n12 = d->shape[1] * d->shape[2];
+        const size_t n = static_cast<size_t>((d->a0_end - d->a0_begin) * n12);
+        float *dm = nullptr, *de = nullptr;
+        SF_CUDA(cudaMalloc(&dm, sizeof(float) * n));
+        std::unique_ptr<float, decltype(&cudaFree)> gm(dm, &cudaFree);
+        SF_CUDA(cudaMalloc(&de, sizeof(float) * n));
+        std::unique_ptr<float, decltype(&cudaFree)> ge(de, &cudaFree);
+        sfb::smooth_medium_run(*d, 1, &lo, &hi, dm, de, d->shape[2], n12, nullptr);
+        SF_CUDA(cudaMemcpy(m, dm, sizeof(float) * n, cudaMemcpyDeviceToHost));
+        SF_CUDA(cudaMemcpy(eta, de, sizeof(float) * n, cudaMemcpyDeviceToHost));
+    });
+}
+
+int sf_plan_set_smooth_medium(sf_plan* p, const sf_smooth_medium_desc* d, double lo, double hi) {
+    if (!p || !d) return SF_ERR_INVALID;
+    return sfb::medium_guard([&] {
+        if (p->kind == sf_plan::DIFFUSION || p->ndim != 3 || !p->m || !p->eta)
+            throw sfb::Status(SF_ERR_INVALID, "smooth medium needs a 3D acoustic or FWI plan");
+        if (d->shape[1] != p->n[1] || d->shape[2] != p->n[2] || d->shape[0] != p->global_n0)
+            throw sfb::Status(SF_ERR_INVALID, "smooth medium: global shape does not match the plan");
+        SF_CUDA(cudaSetDevice(p->device));
+        sf_smooth_medium_desc dd = *d;
+        dd.a0_begin = p->plane0;
+        dd.a0_end = p->plane0 + p->n[0];
+        sfb::smooth_medium_run(dd, 1, &lo, &hi, p->m, p->eta, p->pitch, p->plane, p->stream);
+        ++p->eta_gen;
+    });
 }
 
 int sf_acoustic_constants(int ndim, int order, int forward, double dt, double spacing,

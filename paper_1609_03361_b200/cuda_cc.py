@@ -805,8 +805,12 @@ static size_t extent_bytes(const void* p, size_t row) {{
     return row ? n / row * row : n;
 }}
 
-// powf with a non-integral exponent (codegen.cpp:170-176): evaluated in double
-// and rounded once, as glibc's powf does
+// powf with a non-integral exponent (codegen.cpp:170-176): CUDA's double pow
+// (<= 2 ulp) rounded once to float. glibc's powf (what the gcc build calls)
+// is not always the correctly rounded result either, and double pow is left
+// to CUDA's pow, so operators that use pow / powf are the one KNOWN
+// non-bitwise case of this generic back end (the acoustic and diffusion hot
+// paths have none; DESIGN.md section 9).
 __device__ __forceinline__ float sf_powf(float a, float b) {{
     return (float)pow((double)a, (double)b);
 }}

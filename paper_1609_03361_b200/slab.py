@@ -116,12 +116,13 @@ class SlabRun:
     """One slab of an acoustic run: a slab plan plus its local buffers.
 
     `field` (3 slots), m, eta are the global arrays (only this slab's planes
-    are read); src/rec series, cell indices and weights are global too and
+    are read; with local_medium=True m / eta hold just the local planes); src/rec series, cell indices and weights are global too and
     are filtered/translated here.
     """
 
     def __init__(self, part: SlabPartition, shape, space_order, forward, nt, dt, spacing, m, eta,
-                 src, src_ci, src_w, rec, rec_ci, rec_w, u=None, device=0):
+                 src, src_ci, src_w, rec, rec_ci, rec_w, u=None, device=0,
+                 local_medium=False):
         from . import _lib
         from .api import check
         self.part = part
@@ -166,8 +167,15 @@ class SlabRun:
         self.plan = plan
         u_loc = (np.zeros((3,) + lshape, np.float32) if u is None
                  else np.ascontiguousarray(u[:, sl], np.float32))
-        self.bufs = [u_loc, np.ascontiguousarray(m[sl], np.float32),
-                     np.ascontiguousarray(eta[sl], np.float32), s_ser, s_ci, s_w, r_ser, r_ci, r_w]
+        if local_medium:  # m / eta already hold just this slab's planes
+            if m.shape[0] != part.local_n0 or eta.shape[0] != part.local_n0:
+                raise ValueError("local medium must hold the slab's local planes")
+            m_loc, eta_loc = m, eta
+        else:
+            m_loc, eta_loc = m[sl], eta[sl]
+        self.bufs = [u_loc, np.ascontiguousarray(m_loc, np.float32),
+                     np.ascontiguousarray(eta_loc, np.float32), s_ser, s_ci, s_w, r_ser, r_ci,
+                     r_w]
         argv = (C.c_void_p * 9)(*[b.ctypes.data for b in self.bufs])
         check(_lib.lib.sf_plan_upload(self.plan, argv, 9))
 

@@ -73,6 +73,12 @@ class Port:
         lib.sfp_fwi_adjoint_gradient.argtypes = [
             C.POINTER(SfpAcousticCoefs), _i64p, C.c_int64, _f32p, _f32p, _f32p, _f32p,
             _f32p, _i32p, _f32p, C.c_int64, _f32p, _i32p, _f32p, C.c_int64, _f32p, C.c_int]
+        lib.sfp_smooth_taps.argtypes = [C.c_double, _f64p]
+        lib.sfp_smooth_extrema.argtypes = [_i64p, C.c_int64, C.c_int64, C.c_uint64, C.c_double,
+                                           C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        lib.sfp_smooth_medium.argtypes = [_i64p, C.c_int64, C.c_int64, C.c_uint64, C.c_double,
+                                          C.c_double, C.c_double, C.c_int, C.c_double, C.c_double,
+                                          C.c_double, C.c_double, _f32p, _f32p]
         lib.sfp_diffusion_coefs.argtypes = [SfpRat, SfpRat, C.c_int, C.POINTER(C.c_float),
                                             C.POINTER(C.c_int), C.POINTER(C.c_float)]
         lib.sfp_diffusion_dt.argtypes = [SfpRat, SfpRat, C.c_int, C.POINTER(SfpRat)]
@@ -124,6 +130,25 @@ class Port:
         self.lib.sfp_medium_from_velocity(len(shape), shape, boundary_width, spacing, v_min,
                                           np.ascontiguousarray(v, np.float64).reshape(-1),
                                           m.reshape(-1), eta.reshape(-1))
+        return m, eta
+
+    def smooth_extrema(self, shape, b, e, seed, sigma=8.0):
+        lo, hi = C.c_double(), C.c_double()
+        rc = self.lib.sfp_smooth_extrema(np.asarray(shape, np.int64), b, e, seed, sigma,
+                                         C.byref(lo), C.byref(hi))
+        assert rc == 0, rc
+        return lo.value, hi.value
+
+    def smooth_medium(self, shape, b, e, seed, lo, hi, sigma=8.0, v_lo=1500.0, v_hi=4500.0,
+                      boundary_width=40, spacing=10.0, v_min=1500.0):
+        """m, eta of global planes [b, e) (csrc/medium.cu's definition)."""
+        out = (e - b, shape[1], shape[2])
+        m = np.zeros(out, np.float32)
+        eta = np.zeros(out, np.float32)
+        rc = self.lib.sfp_smooth_medium(np.asarray(shape, np.int64), b, e, seed, sigma, v_lo,
+                                        v_hi, boundary_width, spacing, v_min, lo, hi,
+                                        m.reshape(-1), eta.reshape(-1))
+        assert rc == 0, rc
         return m, eta
 
     # -- runs --------------------------------------------------------------

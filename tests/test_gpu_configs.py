@@ -1,0 +1,241 @@
+"""BASELINE configs at their own layouts, through the CUDA path's public API.
+
+The north star asks every config to match the CPU reference "after the full
+time loop". Each test here builds the config exactly as bench.py does (grid,
+order, dt, medium, sources, receivers: bench.workload) and compares every
+field slot and trace bitwise with the checker:
+
+  C1  2048^2 diffusion, all 500 steps, vs the live reference (oracle/_ref)
+  C2  281^3 order 4, all 625 steps, vs the live reference (acoustic_build +
+      Operator::apply of stencilforge itself; acceptance.cpp:319-361 pins
+      whole buffers the same way)
+  C3  512^3 orders 4 and 12, 65,536 receivers, smooth medium, 5 steps from a
+      random non-zero state, vs the C restatement (pinned to the reference in
+      test_oracle_pin.py)
+  C4  1024^3 order 8, its 8 seeded sources and smooth medium, 3 steps from a
+      random state, vs the C restatement; and the 2-slab in-process chain at
+      C4's per-slab size (2048 x 1024 x 1024 global) vs the C restatement
+  C5  301^3 order 8 FWI with 201 x 201 residual injection (40,401 injectors on
+      grid nodes: colliding corners, zero weights; the grid-wide injection
+      kernel path), 12 steps, vs the port's forward_history + adjoint_gradient
+"""
+import gc
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+def rel_l2(a, b):
+    a = a.astype(np.float64)
+    b = b.astype(np.float64)
+    n = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (n if n > 0 else 1.0)
+
+
+def assert_parity(got, want, what=""):
+    assert got.shape == want.shape, what
+    assert rel_l2(got, want) <= 1e-5, what
+    assert np.array_equal(bits(got), bits(want)), \
+        f"{what}: not bitwise, max abs diff {np.abs(got.astype(np.float64) - want).max()}"
+
+
+@pytest.fixture(scope="module")
+def sf():
+    import paper_1609_03361_b200 as sf
+    if sf._lib.lib.sf_device_count() < 1:
+        pytest.fail("no CUDA device: the GPU tests need a B200")
+    return sf
+
+
+def workload(sf, name, world=1):
+    import bench
+    return bench.workload(name, world, bench.product_stable_dt(sf))
+
+
+def model_of(sf, w, nt=None):
+    return sf.AcousticModel(shape=w.shape, boundary_width=w.bw, spacing=w.h,
+                            nt=w.nt if nt is None else nt, dt=w.dt, space_order=w.order,
+                            f0=w.f0, v_top=w.v_top, v_bottom=w.v_bottom,
+                            src_coords=w.src_coords, rec_coords=w.rec_coords)
+
+
+def smooth_of(sf, w):
+    s = w.smooth
+    return sf.SmoothMedium(shape=w.shape, seed=s["seed"], sigma=s["sigma"], v_lo=s["v_lo"],
+                           v_hi=s["v_hi"], boundary_width=w.bw, spacing=w.h, v_min=s["v_min"])
+
+
+def test_c1_full_time_loop_vs_reference(sf, ref):
+    from fractions import Fraction
+
+    from oracle_lib import ref_diffusion
+    n, nt = 2048, 500
+    rng = np.random.default_rng(2016)  # bench.py's C1 input
+    u0 = np.zeros((n, n), np.float32)
+    u0[1:-1, 1:-1] = rng.random((n - 2, n - 2))
+    cfg = sf.DiffusionConfig(nx=n, ny=n, alpha=Fraction(1, 2), dx=Fraction(1, n - 1),
+                             dy=Fraction(1, n - 1), nt=nt, order=2)
+    b = sf.make_diffusion_operator(cfg)
+    b.u.data[0] = u0
+    b.u.data[1] = u0
+    b.op.apply()
+    ref.set_threads(ref.max_threads())
+    op = ref_diffusion(ref, n, n, (1, 2), (1, n - 1), nt, 2)
+    op.set("u", np.stack([u0, u0]))
+    op.build()
+    op.apply()
+    assert_parity(b.u.data, op.get("u", np.float32, (2, n, n)), "c1 slots")
+
+
+def test_c2_full_time_loop_vs_reference(sf, ref):
+    from oracle_lib import AcousticCase, ref_acoustic
+    w = workload(sf, "c2")
+    assert w.nt == 625 and w.shape == (281, 281, 281) and abs(w.dt - 0.0016) < 1e-15
+    s = sf.acoustic_forward(model_of(sf, w))
+    ref.set_threads(ref.max_threads())
+    op = ref_acoustic(ref, AcousticCase(shape=w.shape, nt=w.nt, boundary_width=w.bw,
+                                        spacing=w.h, dt=w.dt, space_order=w.order, f0=w.f0,
+                                        v_top=w.v_top, v_bottom=w.v_bottom,
+                                        src_coords=w.src_coords, rec_coords=w.rec_coords), True)
+    op.build()
+    op.apply()
+    u = op.get("u", np.float32, (3,) + w.shape)
+    assert np.abs(u).max() > 0
+    assert_parity(s.field.data, u, "c2 slots")
+    assert_parity(s.rec.data.data, op.get("rec", np.float32, (w.nt, len(w.rec_coords))),
+                  "c2 receivers")
+    assert_parity(s.m.data, op.get("m", np.float32, w.shape), "c2 m")
+    assert_parity(s.eta.data, op.get("eta", np.float32, w.shape), "c2 eta")
+
+
+def _layout_vs_port(sf, port, name, nt, seed):
+    w = workload(sf, name)
+    model = model_of(sf, w, nt)
+    s = sf.acoustic_build(model, True, smooth=smooth_of(sf, w))
+    rng = np.random.default_rng(seed)
+    # a non-zero state so every point of every slot matters
+    u0 = (1e-3 * rng.standard_normal((3,) + w.shape, dtype=np.float32))
+    s.field.data[...] = u0
+    s.op.apply()
+    u = u0
+    rec = np.zeros((nt, len(w.rec_coords)), np.float32)
+    coefs = port.coefs(3, w.order, True, w.dt, w.h)
+    port.acoustic_run(coefs, u, s.m.data, s.eta.data, s.src.data.data.copy(), s.src.ci.data,
+                      s.src.w.data, rec, s.rec.ci.data, s.rec.w.data, nt)
+    assert_parity(s.field.data, u, f"{name} slots")
+    assert_parity(s.rec.data.data, rec, f"{name} receivers")
+    # the smooth medium the plan used is the configured one
+    v = 1.0 / np.sqrt(s.m.data[::37, ::41, ::43].astype(np.float64))
+    assert 1499.0 < v.min() and v.max() < 4501.0 and v.max() - v.min() > 1000.0
+    return s
+
+
+@pytest.mark.parametrize("name", ["c3o4", "c3o12"])
+def test_c3_layout_vs_port(sf, port, name):
+    _layout_vs_port(sf, port, name, 5, 3)
+    gc.collect()
+
+
+def test_c4_layout_vs_port(sf, port):
+    s = _layout_vs_port(sf, port, "c4", 3, 4)
+    assert s.src.np == 8 and s.field.data.shape == (3, 1024, 1024, 1024)
+    del s
+    gc.collect()
+
+
+def test_c4_two_slab_chain_vs_port(sf, port):
+    """Two 1024-plane depth slabs of C4 (global 2048 x 1024 x 1024 -- past the
+    2^31-element limit of one plan, which is what the decomposition is for),
+    each slab generating its own planes of the smooth medium from global
+    indices, in an in-process chain (halo copies device to device): every
+    owned plane and every trace bitwise the C restatement's single-domain
+    run, 3 steps from a state that is random around the slab boundary."""
+    from paper_1609_03361_b200.slab import SlabPartition, SlabRun, chain_run
+    w = workload(sf, "c4", world=2)
+    nt, r = 3, w.order // 2
+    assert w.shape == (2048, 1024, 1024)
+    sm = smooth_of(sf, w)
+    lo, hi = sm.extrema()
+    m, eta = sm.generate(lo, hi)
+    rng = np.random.default_rng(12)
+    u = np.zeros((3,) + w.shape, np.float32)
+    band = slice(1024 - 40, 1024 + 40)
+    u[:, band] = 1e-3 * rng.standard_normal((3, 80) + w.shape[1:], dtype=np.float32)
+    src_ci, src_w = port.interp(np.array(w.src_coords), w.h, w.shape)
+    rec_ci, rec_w = port.interp(np.array(w.rec_coords), w.h, w.shape)
+    ser = np.array([port.ricker(w.f0, t * w.dt, 1.0 / w.f0) for t in range(nt)],
+                   np.float32)[:, None].repeat(len(src_ci), axis=1)
+    ext, slabs = [], []
+    for g in range(2):
+        part = SlabPartition.split(w.shape[0], r, 2, g)
+        ext.append(sm.extrema(part.own_begin, part.own_end))
+        m_loc, eta_loc = sm.generate(lo, hi, part.plane0, part.plane_end)
+        assert np.array_equal(bits(m_loc), bits(m[part.local()]))
+        assert np.array_equal(bits(eta_loc), bits(eta[part.local()]))
+        slabs.append(SlabRun(part, w.shape, w.order, True, nt, w.dt, w.h, m_loc, eta_loc, ser,
+                             src_ci, src_w, np.zeros((nt, len(rec_ci)), np.float32), rec_ci,
+                             rec_w, u=u, local_medium=True))
+        del m_loc, eta_loc
+    assert min(e[0] for e in ext) == lo and max(e[1] for e in ext) == hi
+    chain_run(slabs, 0, nt)
+    rec = np.zeros((nt, len(rec_ci)), np.float32)
+    port.acoustic_run(port.coefs(3, w.order, True, w.dt, w.h), u, m, eta, ser.copy(), src_ci,
+                      src_w, rec, rec_ci, rec_w, nt)
+    del m, eta
+    for sl in slabs:
+        bufs = sl.download()
+        p = sl.part
+        assert np.array_equal(bits(bufs[0][:, p.owned_local()]),
+                              bits(u[:, p.own_begin:p.own_end])), f"slab {p.rank}"
+        if len(sl.rec_idx):
+            assert np.array_equal(bits(bufs[6][:, :len(sl.rec_idx)]), bits(rec[:, sl.rec_idx]))
+        sl.close()
+        del bufs
+    assert np.abs(u[:, band]).max() > 0
+    del u, slabs
+    gc.collect()
+
+
+def test_c5_layout_vs_port(sf, port):
+    import bench
+    shape, order, nt = (301, 301, 301), 8, 12
+    bw, h = bench.BW, bench.H
+    dt = min(0.4 * h / 4500.0, sf.api._stable_dt(3, order, h, 4500.0, 4500.0))
+    sm = sf.SmoothMedium(shape=shape, boundary_width=bw, spacing=h,
+                         **{k: v for k, v in bench.SMOOTH.items()})
+    lo, hi = sm.extrema()
+    m, eta = sm.generate(lo, hi)
+    mid = shape[1] // 2
+    src_c = np.array([[(bw + 2) * h, mid * h, mid * h]])
+    rec_c = np.array([[(bw + 10) * h, (bw + i) * h, (bw + j) * h]
+                      for i in range(201) for j in range(201)])
+    src_ci, src_w = port.interp(src_c, h, shape)
+    rec_ci, rec_w = port.interp(rec_c, h, shape)
+    assert (rec_w == 0).sum() > 7 * len(rec_c) - 1  # receivers on grid nodes: one weight each
+    rng = np.random.default_rng(5)
+    src = np.array([port.ricker(10.0, t * dt, 0.1) for t in range(nt)], np.float32)[:, None]
+    residual = rng.standard_normal((nt, len(rec_c)), dtype=np.float32)
+    plan = sf.FwiPlan(shape, order, nt, dt, h, 1, len(rec_c))
+    rec_out, grad, v, srcs = plan.gradient(m, eta, src, src_ci, src_w, rec_ci, rec_w, residual,
+                                           want_v=True, want_src=True)
+    cf = port.coefs(3, order, True, dt, h)
+    hist = np.zeros((nt + 2,) + shape, np.float32)
+    rec = np.zeros((nt, len(rec_c)), np.float32)
+    port.forward_history(cf, hist, m, eta, src, src_ci, src_w, rec, rec_ci, rec_w, nt)
+    assert_parity(rec_out, rec, "c5 forward traces")
+    ca = port.coefs(3, order, False, dt, h)
+    vv = np.zeros((3,) + shape, np.float32)
+    g = np.zeros(shape, np.float32)
+    s2 = np.zeros((nt, 1), np.float32)
+    port.adjoint_gradient(ca, vv, m, eta, hist, residual, rec_ci, rec_w, s2, src_ci, src_w, g,
+                          nt)
+    assert np.abs(g).max() > 0
+    assert_parity(v, vv, "c5 adjoint slots")
+    assert_parity(srcs, s2, "c5 adjoint source traces")
+    assert_parity(grad, g, "c5 gradient")

@@ -545,48 +545,6 @@ def test_step_ranges_and_tile_edge_points(sf, port, order, shape, forward, split
     assert_parity(bufs[6] if forward else bufs[3], want_rec if forward else want_src)
 
 
-def test_bench_helpers(sf):
-    """bench_acoustic / bench_diffusion: the reference's restore-and-median
-    protocol; the sweep reports every kernel configuration and leaves the
-    operator producing the oracle's result."""
-    from paper_1609_03361_b200.benchmarks import bench_acoustic, bench_diffusion, format_bench
-    model = sf.AcousticModel(shape=(36, 40, 44), nt=6, boundary_width=4, space_order=4)
-    lines = bench_acoustic(model, runs=2)
-    assert lines[0].variant == "apply" and lines[0].median_s > 0
-    assert any(l.variant == "resident" and "vector-tma" in l.plan for l in lines)
-    assert all(l.median_s > 0 for l in lines)
-    d = bench_diffusion(sf.DiffusionConfig(nx=64, ny=64, nt=10), runs=2)
-    assert d[0].scenario == "diffusion" and d[0].median_s > 0
-    assert format_bench(lines + d).count("\n") == len(lines) + 1
-
-
-@pytest.mark.parametrize("cfg", ["c2", "c3o8", "c3o16"])
-def test_full_size_config_bitwise(sf, port, cfg):
-    """BASELINE-size grids (C2 281^3 order 4; C3 512^3 orders 8 and 16) with
-    the bench's sources and receivers, a seeded random medium, 3 time steps
-    from a non-zero state: every slot and trace bitwise the oracle's (the
-    kernels, tiles, fused epilogue and chunking of the timed configurations)."""
-    import bench
-    model, _, _ = bench.make_model(cfg)
-    model.nt = 3
-    shape = tuple(model.shape)
-    rng = np.random.default_rng(11)
-    v = (1500.0 + 3000.0 * rng.random(shape)).astype(np.float64)
-    s = sf.acoustic_forward(model, v_field=v, v_min=1500.0)
-    # restart from a non-zero state so every slot matters
-    u0 = (1e-3 * rng.standard_normal((3,) + shape)).astype(np.float32)
-    s.field.data[...] = u0
-    s.rec.data.data[...] = 0
-    s.op.apply()
-    coefs = port.coefs(3, model.space_order, True, model.dt, model.spacing)
-    u = u0.copy()
-    rec = np.zeros_like(s.rec.data.data)
-    port.acoustic_run(coefs, u, s.m.data, s.eta.data, s.src.data.data.copy(), s.src.ci.data,
-                      s.src.w.data, rec, s.rec.ci.data, s.rec.w.data, model.nt)
-    assert np.array_equal(bits(s.field.data), bits(u))
-    assert np.array_equal(bits(s.rec.data.data), bits(rec))
-
-
 @pytest.mark.parametrize("shape,order,ns,nr,nt", [
     ((9, 9, 9), 8, 1, 1, 1),        # interior of a single point per axis
     ((10, 40, 70), 8, 0, 3, 4),     # no sources

@@ -177,16 +177,6 @@ def test_invalid_orders_and_shapes():
         sf.Grid().create_dense("m", (4, 10), 4)
 
 
-def test_format_bench_matches_reference_text():
-    # bench.cpp:121-133: "bench scenario=%s variant=%s plan=%s runs=%d median_s=%.6f\n"
-    from paper_1609_03361_b200.benchmarks import BenchLine, format_bench
-    txt = format_bench([BenchLine("acoustic", "apply", "default", 3, 0.0123456789),
-                        BenchLine("acoustic", "apply", "SkippedTooLarge", 0, 0.0)])
-    assert txt == ("bench scenario=acoustic variant=apply plan=default runs=3 median_s=0.012346\n"
-                   "bench scenario=acoustic variant=apply plan=SkippedTooLarge runs=0 "
-                   "median_s=0.000000\n")
-
-
 def test_reference_arm_line_on_cpu():
     """bench.py --impl reference (the driver's reference arm) runs the
     reference's own CPU path and prints the contract's JSON line; C1 is the

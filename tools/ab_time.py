@@ -7,7 +7,7 @@ plan in ONE process, and the variants' full time loops are timed round-robin,
 so they see the same thermal / power state; the median per variant is
 reported. Usage:
 
-    python -m paper_1609_03361_b200.ab_time c2 20 "SF_VEC_RPL=1" "SF_VEC_RPL=2"
+    python tools/ab_time.py c2 20 "SF_VEC_RPL=1" "SF_VEC_RPL=2"
 """
 import json
 import os
@@ -23,26 +23,27 @@ def main():
     rounds = int(sys.argv[2])
     variants = sys.argv[3:]
     import paper_1609_03361_b200 as sf
-    model, v, vmin = bench.make_model(cfg)
-    pts = bench.interior_points(model)
+    w = bench.workload(cfg, 1, bench.product_stable_dt(sf))
+    nt = w.nt
+    pts = bench.interior_points(w.shape, w.order)
     plans = []
     for var in variants:
         saved = dict(os.environ)
         for kv in filter(None, var.split(",")):
             k, val = kv.split("=", 1)
             os.environ[k] = val
-        s = sf.acoustic_build(model, True, v_field=v, v_min=vmin)
+        s = bench.b200_setup(sf, w)
         os.environ.clear()
         os.environ.update(saved)
         s.op.upload()
-        s.op.run(0, model.nt)
+        s.op.run(0, nt)
         s.op.synchronize()
         plans.append(s)
     times = [[] for _ in variants]
     for _ in range(rounds):
         for i, s in enumerate(plans):
             tot, _, _ = s.op.time(stencil=False)
-            times[i].append(tot / model.nt * 1e3)
+            times[i].append(tot / nt * 1e3)
     for var, t in zip(variants, times):
         med = statistics.median(t)
         print(json.dumps({"cfg": cfg, "variant": var, "us_per_step_median": med,

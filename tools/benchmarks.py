@@ -21,7 +21,11 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import api
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1609_03361_b200 import api  # noqa: E402
 
 
 @dataclass

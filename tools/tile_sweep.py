@@ -14,14 +14,13 @@ def main():
     tiles = sys.argv[3].split(";") if len(sys.argv) > 3 else [
         "1,8", "1,16", "2,8", "2,16", "3,8", "3,16", "4,8", "4,16"]
     import paper_1609_03361_b200 as sf
-    model, v, vmin = bench.make_model(cfg)
-    model.nt = nt
-    pts = bench.interior_points(model)
+    w = bench.workload(cfg, 1, bench.product_stable_dt(sf))
+    pts = bench.interior_points(w.shape, w.order)
     out = []
     for t in tiles:
         os.environ["SF_TILE"] = t
         try:
-            s = sf.acoustic_build(model, True, v_field=v, v_min=vmin)
+            s = bench.b200_setup(sf, w, nt=nt)
         except Exception as e:  # tile not compiled for this order
             print(cfg, t, "skip", e)
             continue
