@@ -24,10 +24,11 @@ import numpy as np
 import pytest
 
 
-def _blob(shape, scale):
-    idx = np.indices(shape, dtype=np.float64)
-    c = (np.array(shape, np.float64) / 2.0)[:, None, None, None]
-    return np.exp(-((idx - c) ** 2).sum(0) / scale)
+def _blob(shape, scale, center=None):
+    """exp(-|x - center|^2 / scale), centre of the grid by default (separable)."""
+    c = np.array(shape, np.float64) / 2.0 if center is None else np.asarray(center, np.float64)
+    g = [np.exp(-(np.arange(n, dtype=np.float64) - c[a]) ** 2 / scale) for a, n in enumerate(shape)]
+    return g[0][:, None, None] * g[1][None, :, None] * g[2][None, None, :]
 
 
 def _taylor(J, J0, gdm, dm_scale=1.0):
@@ -96,7 +97,7 @@ def test_port_gradient_taylor(port):
 def test_gpu_gradient_taylor_c5_layout():
     import bench
     import paper_1609_03361_b200 as sf
-    shape, order, nt = (301, 301, 301), 8, 300
+    shape, order, nt = (301, 301, 301), 8, 500
     bw, h = bench.BW, bench.H
     dt = min(0.4 * h / 4500.0, sf.api._stable_dt(3, order, h, 4500.0, 4500.0))
     sm = sf.SmoothMedium(shape=shape, boundary_width=bw, spacing=h,
@@ -119,19 +120,21 @@ def test_gpu_gradient_taylor_c5_layout():
     def traces(mm):
         rec, _, _, _ = plan.gradient(mm, eta, src, sci, sw, rci, rw, zero)
         return rec
-    dobs = traces((m * (1 + 0.05 * _blob(shape, 900.0))).astype(np.float32)).astype(np.float64)
+    # the model error and the perturbation sit where the first arrivals and
+    # their reflections reach the receivers within nt: a few tens of cells
+    # below the source (a perturbation the data cannot see in nt steps would
+    # leave J flat to first order and the test vacuous)
+    dobs = traces((m * (1 + 0.05 * _blob(shape, 200.0, (bw + 24, mid + 8, mid - 6))))
+                  .astype(np.float32)).astype(np.float64)
     d0 = traces(m)
     J0 = 0.5 * float(((d0 - dobs) ** 2).sum())
     assert J0 > 0
     res = (d0 - dobs).astype(np.float32)
     rec_out, grad, _, _ = plan.gradient(m, eta, src, sci, sw, rci, rw, res)
     assert np.array_equal(rec_out, d0)
-    rng = np.random.default_rng(3)
-    dm = (rng.standard_normal(shape, dtype=np.float32) * m * 0.01).astype(np.float32)
-    mask = np.zeros(shape, bool)
-    mask[bw:-bw, bw:-bw, bw:-bw] = True
-    dm[~mask] = 0
+    dm = (m * 0.01 * _blob(shape, 120.0, (bw + 20, mid, mid))).astype(np.float32)
     gdm = -float((grad.astype(np.float64) * dm).sum())
+    assert abs(gdm) > 1e-3 * J0
 
     def J(hh):
         d = traces((m + hh * dm).astype(np.float32)).astype(np.float64)
