@@ -425,24 +425,31 @@ def product_stable_dt(sf):
 
 
 def roofline_line(ms_per_step, share, nt, pts, eta_skip, r, traffic):
-    """Dominant kernel (the stencil): algorithmic bytes per launch over its
-    average launch time inside the timed region."""
+    """Dominant kernel (the stencil): ALGORITHMIC bytes per launch -- SURVEY
+    §8(d)'s compulsory 20 B per interior point (read u(t), u(t-1), m, eta;
+    write u(t+1)) x the interior points of one launch -- over its average
+    launch time inside the timed region. The kernel moves fewer bytes than
+    that (all-zero eta boxes are never loaded): `moved_bytes_per_launch` and
+    `frac_moved` report that stricter lens, `traffic` the ncu DRAM bytes."""
     stencil_launch_ms = ms_per_step / nt * share
-    alg_bytes = (20 - 4 * eta_skip) * pts
+    alg_bytes = 20.0 * pts
+    moved = (20 - 4 * eta_skip) * pts
     peak, peak_kind = load_peaks()
-    achieved = alg_bytes / (stencil_launch_ms / 1e3) / 1e9
+    secs = stencil_launch_ms / 1e3
+    achieved = alg_bytes / secs / 1e9
     ops = 21 + 13 * r
     return ({"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
              "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
              "kernel": f"3D stencil (radius {r}) avg launch {stencil_launch_ms * 1e3:.1f} us",
-             "alg_bytes_per_launch": alg_bytes, "eta_boxes_skipped": eta_skip,
-             "frac_of_20B": 20 * pts / (stencil_launch_ms / 1e3) / 1e9 / peak},
+             "alg_bytes_per_launch": alg_bytes, "bytes_per_point": 20,
+             "moved_bytes_per_launch": moved, "eta_boxes_skipped": eta_skip,
+             "frac_moved": moved / secs / 1e9 / peak},
             # second lens for the high orders: the reference's exact fp32
             # operation count (no FMA contraction) against 148 SMs x 128 lanes
             {"bound": "fp32", "ops_per_point": ops,
-             "achieved": ops * pts / (stencil_launch_ms / 1e3) / 1e12,
+             "achieved": ops * pts / secs / 1e12,
              "peak": 148 * 128 * 1.965e9 / 1e12, "unit": "Tops/s",
-             "frac": ops * pts / (stencil_launch_ms / 1e3) / (148 * 128 * 1.965e9),
+             "frac": ops * pts / secs / (148 * 128 * 1.965e9),
              "peak_source": "148 SMs x 128 fp32 lanes x 1965 MHz (max SM clock)"})
 
 

@@ -149,6 +149,7 @@ struct sf_plan {
     bool use_vec = false;  // 4 points/thread, LDS.128 variant of the TMA pipeline
     bool use_vecq = false; // ... with the a0 neighbours in a register queue (radius >= 5)
     bool vecq_ring = false;  // ... future a0 planes from a shared-memory core ring (vecq2)
+    bool vecq_unroll = false;  // ... plane loop unrolled over the queue period (vecqu)
     int vec_warps = 8;
     int vec_rpl = 1;  // vector kernel: rows of four points per lane (1 or 2)
     int tma_stages = 4;
@@ -537,10 +538,12 @@ size_t vec_smem_bytes(int r, int warps, int stages, int npme = 3, int nx = 2, in
 }
 
 template <bool FWD>
-const void* vecq_ptr(int r, int warps, bool ring = false) {
+const void* vecq_ptr(int r, int warps, bool ring = false, bool unroll = false) {
 #define SF_V(RR)                                                                               \
     case RR:                                                                                   \
         if (ring && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq2_kernel<RR, FWD, 4>); \
+        if (unroll) return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vecqu_kernel<RR, FWD, 4>) \
+                                      : reinterpret_cast<const void*>(&acoustic3d_vecqu_kernel<RR, FWD, 8>); \
         return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 4>) \
                           : reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 8>);
     switch (r) {
@@ -561,12 +564,16 @@ size_t vecq_smem_bytes(int r, int warps, int stages, bool ring = false) {
 
 template <bool FWD>
 void launch_vecq(int r, int warps, dim3 g, size_t smem, cudaStream_t st, const TmaStencilArgs& A,
-                 bool ring = false) {
+                 bool ring = false, bool unroll = false) {
     const dim3 b(32 * warps);
 #define SF_V(RR)                                                                   \
     case RR:                                                                       \
         if (ring && warps == 4)                                                    \
             acoustic3d_vecq2_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);            \
+        else if (unroll && warps == 4)                                             \
+            acoustic3d_vecqu_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);            \
+        else if (unroll)                                                           \
+            acoustic3d_vecqu_kernel<RR, FWD, 8><<<g, b, smem, st>>>(A);            \
         else if (warps == 4)                                                       \
             acoustic3d_vecq_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);             \
         else                                                                       \
@@ -743,8 +750,8 @@ void setup_tma(Plan& p) {
         p.tma_stages = stages;  // <= 12: barriers + eta flags share 256 bytes
         p.tma_smem = vecq_smem_bytes(r, p.vec_warps, stages, ring);
         for (int fwd = 0; fwd < 2; ++fwd) {
-            const void* fn = fwd ? vecq_ptr<true>(r, p.vec_warps, ring)
-                                 : vecq_ptr<false>(r, p.vec_warps, ring);
+            const void* fn = fwd ? vecq_ptr<true>(r, p.vec_warps, ring, p.vecq_unroll)
+                                 : vecq_ptr<false>(r, p.vec_warps, ring, p.vecq_unroll);
             if (!fn) throw Status(SF_ERR_INVALID, "queue vector stencil not compiled");
             SF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(p.tma_smem)));
@@ -1012,9 +1019,11 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
         if (p.use_vecq) {
             T.cur_core = *mc.pme;
             if (p.ac.forward)
-                launch_vecq<true>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T, p.vecq_ring);
+                launch_vecq<true>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T, p.vecq_ring,
+                                  p.vecq_unroll);
             else
-                launch_vecq<false>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T, p.vecq_ring);
+                launch_vecq<false>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T, p.vecq_ring,
+                                   p.vecq_unroll);
             return;
         }
         if (p.use_vec) {
@@ -1821,8 +1830,8 @@ void set_grid(Plan& p) {
                                    : p.tile_ty;
     int per_sm = 0;
     if (p.use_vecq) {
-        const void* fn = p.ac.forward ? vecq_ptr<true>(r, p.vec_warps, p.vecq_ring)
-                                      : vecq_ptr<false>(r, p.vec_warps, p.vecq_ring);
+        const void* fn = p.ac.forward ? vecq_ptr<true>(r, p.vec_warps, p.vecq_ring, p.vecq_unroll)
+                                      : vecq_ptr<false>(r, p.vec_warps, p.vecq_ring, p.vecq_unroll);
         if (fn)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.vec_warps, p.tma_smem);
     } else if (p.use_vec) {
@@ -1918,6 +1927,8 @@ void enable_tma(Plan& p) {
        // sustained order 12 747 vs 692 us, order 16 798 vs 768 us per step
         const char* e = std::getenv("SF_VECQ2");
         p.vecq_ring = e && e[0] == '1';
+        const char* u = std::getenv("SF_VECQU");
+        p.vecq_unroll = u && u[0] == '1';
     }
     if (const char* env = std::getenv("SF_NO_TMA"))
         if (env[0] == '1') return;
