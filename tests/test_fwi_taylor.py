@@ -44,6 +44,7 @@ def _taylor(J, J0, gdm, dm_scale=1.0):
 
 
 def _check(hs, e1, e2, fd, gdm):
+    print(f"taylor: h={hs} e1={e1} e2={e2} centred_fd={fd} <dJ/dm,dm>={gdm}")
     assert abs(fd / gdm - 1.0) < 0.01, (fd, gdm)
     slopes2 = [np.log2(e2[i] / e2[i + 1]) for i in range(len(hs) - 1)]
     slopes1 = [np.log2(e1[i] / e1[i + 1]) for i in range(len(hs) - 1)]

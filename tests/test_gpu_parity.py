@@ -337,7 +337,8 @@ VARIANTS = [{}, {"SF_VEC": "0"}, {"SF_NO_TMA": "1"}, {"SF_VEC": "0", "SF_TMA": "
             {"SF_VEC_NX": "1", "SF_TMA_STAGES": "4"}, {"SF_NO_FUSED_SPARSE": "1"},
             {"SF_VEC_RPL": "2"}, {"SF_VEC_RPL": "2", "SF_VEC_NX": "1"},
             {"SF_VEC_RPL": "2", "SF_VEC_NX": "2", "SF_VEC_WARPS": "8"}, {"SF_VECQ2": "1"},
-            {"SF_VECQ2": "1", "SF_TMA_STAGES": "3"}]
+            {"SF_VECQ2": "1", "SF_TMA_STAGES": "3"}, {"SF_VECQD": "1"},
+            {"SF_VECQD": "2"}, {"SF_VECQ": "1"}, {"SF_VECQ": "1", "SF_VECQD": "2"}]
 
 
 @pytest.mark.parametrize("order", [2, 6, 8, 12, 16])
@@ -350,6 +351,33 @@ def test_every_kernel_variant_bitwise(sf, port, monkeypatch, order, env):
     shape = (29, 37, 101)
     nt = 9
     c = random_case(port, shape, order, seed=order + 31)
+    rng = c["rng"]
+    src = rng.standard_normal((nt, 3)).astype(np.float32)
+    rec = np.zeros((nt, 17), np.float32)
+    out = run_plan_raw(sf, shape, order, True, c["dt"], 10.0, nt, c["m"], c["eta"], src.copy(),
+                       c["src_ci"], c["src_w"], rec.copy(), c["rec_ci"], c["rec_w"])
+    coefs = port.coefs(3, order, True, c["dt"], 10.0)
+    u = np.zeros((3,) + shape, np.float32)
+    port.acoustic_run(coefs, u, c["m"], c["eta"], src, c["src_ci"], c["src_w"], rec, c["rec_ci"],
+                      c["rec_w"], nt)
+    assert_parity(out[0], u)
+    assert_parity(out[6], rec)
+
+
+@pytest.mark.parametrize("order", [8, 12, 16])
+@pytest.mark.parametrize("zchunks", ["1", "3"])
+@pytest.mark.parametrize("dec", ["1", "2"])
+def test_decoupled_queue_kernel_long_chunks(sf, port, monkeypatch, order, zchunks, dec):
+    """The warp-decoupled queue-vector kernel (SF_VECQD=1/2: per-warp stage
+    releases at the end of the step / after its last shared read, no CTA
+    barrier per step) over a-0 chunks long enough for every stage to be
+    refilled many times, odd and even chunk lengths: bitwise the oracle."""
+    monkeypatch.setenv("SF_VECQD", dec)
+    monkeypatch.setenv("SF_VECQ", "1")  # order 8 on the queue kernel too
+    monkeypatch.setenv("SF_ZCHUNKS", zchunks)
+    shape = (97, 30, 77)
+    nt = 4
+    c = random_case(port, shape, order, seed=order + 7)
     rng = c["rng"]
     src = rng.standard_normal((nt, 3)).astype(np.float32)
     rec = np.zeros((nt, 17), np.float32)
