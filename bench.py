@@ -173,7 +173,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, smax, reasons = [], None, set()
+        sm, smax, reasons, watts = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             p = [x.strip() for x in ln.split(",")]
@@ -184,13 +184,20 @@ class ClockSampler:
                 smax = float(p[1])
             except ValueError:
                 continue
+            try:
+                watts.append(float(p[2]))
+            except ValueError:
+                pass
             for nm, val in zip(names, p[4:8]):
                 if val.lower() == "active":
                     reasons.add(nm)
         if not sm:
             return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
+               "samples": len(sm)}
+        if watts:
+            out["power_w_median"] = float(np.median(watts))
+        return out
 
 
 def dist_init():
@@ -770,16 +777,37 @@ def run_b200_slabs(args, world, rank, local):
         arr = t.numpy()
         arr[...] = a
         return arr, t
-    keep = [pinned(b) for b in slab.bufs]
-    slab.bufs = [k[0] for k in keep]
-    barrier(world)
-    t_e = time.perf_counter()
-    for _ in range(args.steps):
-        argv = (C.c_void_p * 9)(*[b.ctypes.data for b in slab.bufs])
-        sf.api.check(_lib.lib.sf_plan_invoke(slab.plan, argv, 9))
-    e2e_s = reduce_over_ranks(world, (time.perf_counter() - t_e) / args.steps)
-    h2d = reduce_over_ranks(world, float(sum(b.nbytes for b in slab.bufs))) * world
-    d2h = reduce_over_ranks(world, float(slab.bufs[0].nbytes + slab.bufs[6].nbytes)) * world
+    # every rank of the node pins its own slab's nine arrays at once: check
+    # the host has room (a rank replaces its pageable arrays one at a time)
+    need = float(sum(b.nbytes for b in slab.bufs))
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    try:
+        import psutil
+        avail = float(psutil.virtual_memory().available)
+    except Exception:
+        avail = float("inf")
+    room = reduce_over_ranks(world, 1.0 if 1.3 * need * local_world < avail else 0.0, "min")
+    e2e = None
+    if room > 0:
+        keep = []
+        for i in range(len(slab.bufs)):
+            arr, t = pinned(slab.bufs[i])
+            slab.bufs[i] = arr
+            keep.append(t)
+        barrier(world)
+        t_e = time.perf_counter()
+        for _ in range(args.steps):
+            argv = (C.c_void_p * 9)(*[b.ctypes.data for b in slab.bufs])
+            sf.api.check(_lib.lib.sf_plan_invoke(slab.plan, argv, 9))
+        e2e_s = reduce_over_ranks(world, (time.perf_counter() - t_e) / args.steps)
+        h2d = reduce_over_ranks(world, float(sum(b.nbytes for b in slab.bufs))) * world
+        d2h = reduce_over_ranks(world, float(slab.bufs[0].nbytes + slab.bufs[6].nbytes)) * world
+        e2e = {"value": pts * w.nt / e2e_s / 1e9, "unit": "GPts/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+    else:
+        e2e = {"value": None, "unit": "GPts/s",
+               "skipped": f"host memory: {local_world} ranks x {need / 1e9:.1f} GB pinned "
+                          f"exceeds the {avail / 1e9:.0f} GB available"}
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -798,8 +826,7 @@ def run_b200_slabs(args, world, rank, local):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": cfg, "roofline": roof, "compute_roofline": comp,
             "stencil_share": share, "cpu_baseline": base,
-            "e2e": {"value": pts * w.nt / e2e_s / 1e9, "unit": "GPts/s",
-                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "e2e": e2e,
             "gpu_launches": int(nl.value * args.steps),
             "clocks": clocks.summary(),
         }
