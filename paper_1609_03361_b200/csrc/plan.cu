@@ -149,7 +149,6 @@ struct sf_plan {
     bool use_vec = false;  // 4 points/thread, LDS.128 variant of the TMA pipeline
     bool use_vecq = false; // ... with the a0 neighbours in a register queue (radius >= 5)
     bool vecq_ring = false;  // ... future a0 planes from a shared-memory core ring (vecq2)
-    int vecq_dec = 0;  // ... warps decoupled by per-warp stage releases (no CTA barrier)
     int vec_warps = 8;
     int vec_rpl = 1;  // vector kernel: rows of four points per lane (1 or 2)
     int tma_stages = 4;
@@ -538,16 +537,14 @@ size_t vec_smem_bytes(int r, int warps, int stages, int npme = 3, int nx = 2, in
 }
 
 template <bool FWD>
-const void* vecq_ptr(int r, int warps, bool ring = false, int dec = 0) {
+const void* vecq_ptr(int r, int warps, bool ring = false) {
 #define SF_V(RR)                                                                               \
     case RR:                                                                                   \
         if (ring && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq2_kernel<RR, FWD, 4>); \
-        if (dec == 1 && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 4, 1>); \
-        if (dec == 2 && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 4, 2>); \
         return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 4>) \
                           : reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 8>);
     switch (r) {
-        SF_V(3) SF_V(4) SF_V(5) SF_V(6) SF_V(7) SF_V(8)
+        SF_V(5) SF_V(6) SF_V(7) SF_V(8)
         default: return nullptr;
     }
 #undef SF_V
@@ -564,24 +561,20 @@ size_t vecq_smem_bytes(int r, int warps, int stages, bool ring = false) {
 
 template <bool FWD>
 void launch_vecq(int r, int warps, dim3 g, size_t smem, cudaStream_t st, const TmaStencilArgs& A,
-                 bool ring = false, int dec = 0) {
+                 bool ring = false) {
     const dim3 b(32 * warps);
 #define SF_V(RR)                                                                   \
     case RR:                                                                       \
         if (ring && warps == 4)                                                    \
             acoustic3d_vecq2_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);            \
-        else if (dec == 1 && warps == 4)                                           \
-            acoustic3d_vecq_kernel<RR, FWD, 4, 1><<<g, b, smem, st>>>(A);          \
-        else if (dec == 2 && warps == 4)                                           \
-            acoustic3d_vecq_kernel<RR, FWD, 4, 2><<<g, b, smem, st>>>(A);          \
         else if (warps == 4)                                                       \
             acoustic3d_vecq_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);             \
         else                                                                       \
             acoustic3d_vecq_kernel<RR, FWD, 8><<<g, b, smem, st>>>(A);             \
         return;
     switch (r) {
-        SF_V(3) SF_V(4) SF_V(5) SF_V(6) SF_V(7) SF_V(8)
-        default: throw Status(SF_ERR_INVALID, "queue vector stencil compiled for radius 3..8");
+        SF_V(5) SF_V(6) SF_V(7) SF_V(8)
+        default: throw Status(SF_ERR_INVALID, "queue vector stencil compiled for radius 5..8");
     }
 #undef SF_V
 }
@@ -750,8 +743,8 @@ void setup_tma(Plan& p) {
         p.tma_stages = stages;  // <= 12: barriers + eta flags share 256 bytes
         p.tma_smem = vecq_smem_bytes(r, p.vec_warps, stages, ring);
         for (int fwd = 0; fwd < 2; ++fwd) {
-            const void* fn = fwd ? vecq_ptr<true>(r, p.vec_warps, ring, p.vecq_dec)
-                                 : vecq_ptr<false>(r, p.vec_warps, ring, p.vecq_dec);
+            const void* fn = fwd ? vecq_ptr<true>(r, p.vec_warps, ring)
+                                 : vecq_ptr<false>(r, p.vec_warps, ring);
             if (!fn) throw Status(SF_ERR_INVALID, "queue vector stencil not compiled");
             SF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(p.tma_smem)));
@@ -1019,11 +1012,9 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
         if (p.use_vecq) {
             T.cur_core = *mc.pme;
             if (p.ac.forward)
-                launch_vecq<true>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T, p.vecq_ring,
-                                  p.vecq_dec);
+                launch_vecq<true>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T, p.vecq_ring);
             else
-                launch_vecq<false>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T, p.vecq_ring,
-                                   p.vecq_dec);
+                launch_vecq<false>(p.ac.radius, p.vec_warps, grid3, p.tma_smem, p.stream, T, p.vecq_ring);
             return;
         }
         if (p.use_vec) {
@@ -1830,8 +1821,8 @@ void set_grid(Plan& p) {
                                    : p.tile_ty;
     int per_sm = 0;
     if (p.use_vecq) {
-        const void* fn = p.ac.forward ? vecq_ptr<true>(r, p.vec_warps, p.vecq_ring, p.vecq_dec)
-                                      : vecq_ptr<false>(r, p.vec_warps, p.vecq_ring, p.vecq_dec);
+        const void* fn = p.ac.forward ? vecq_ptr<true>(r, p.vec_warps, p.vecq_ring)
+                                      : vecq_ptr<false>(r, p.vec_warps, p.vecq_ring);
         if (fn)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.vec_warps, p.tma_smem);
     } else if (p.use_vec) {
@@ -1927,17 +1918,13 @@ void enable_tma(Plan& p) {
        // sustained order 12 747 vs 692 us, order 16 798 vs 768 us per step
         const char* e = std::getenv("SF_VECQ2");
         p.vecq_ring = e && e[0] == '1';
-        const char* u = std::getenv("SF_VECQD");
-        p.vecq_dec = u ? std::atoi(u) : 0;
     }
     if (const char* env = std::getenv("SF_NO_TMA"))
         if (env[0] == '1') return;
     const char* vec = std::getenv("SF_VEC");
     const bool vec_on = !(vec && vec[0] == '0');
     const char* vq = std::getenv("SF_VECQ");
-    // SF_VECQ=1: the queue-vector kernels at radius 3..4 too (experiments)
-    const bool vq_low = vq && vq[0] == '1' && p.ac.radius >= 3 && p.kind != Plan::FWI;
-    if (vec_on && p.ac.radius <= 4 && !vq_low) {
+    if (vec_on && p.ac.radius <= 4) {
         p.use_vec = true;
         // FWI: the forward runs the same tile choice as a plain forward plan;
         // the 4-warp gradient kernel has its own maps (setup_tma)
@@ -1974,7 +1961,7 @@ void enable_tma(Plan& p) {
         set_grid(p);
         return;
     }
-    if (vec_on && (p.ac.radius >= 5 || vq_low) && !(vq && vq[0] == '0')) {
+    if (vec_on && p.ac.radius >= 5 && !(vq && vq[0] == '0')) {
         p.use_vec = true;
         p.use_vecq = true;
         p.vec_warps = 4;
