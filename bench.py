@@ -207,6 +207,23 @@ def dist_init():
     return world, rank, local
 
 
+class stdout_to_stderr:
+    """File descriptor 1 -> 2 for a block: library banners (NCCL prints its
+    version at communicator init on some setups) must not land on stdout,
+    which carries exactly one JSON line from rank 0."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *a):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 def dist_start(local):
     import torch
     import torch.distributed as dist
@@ -746,7 +763,8 @@ def run_b200_slabs(args, world, rank, local):
     obj = [nccl_unique_id() if rank == 0 else None]
     if world > 1:
         dist.broadcast_object_list(obj, src=0)
-    slab.attach_nccl(obj[0], world, rank)
+    with stdout_to_stderr():
+        slab.attach_nccl(obj[0], world, rank)
     for _ in range(args.warmup):
         slab.run(0, w.nt)
     barrier(world)
@@ -851,13 +869,17 @@ def main():
     ap.add_argument("--force-slabs", action="store_true")
     args = ap.parse_args()
     world, rank, local = dist_init()
+    if rank != 0:  # only rank 0 writes stdout (its one JSON line)
+        sys.stdout.flush()
+        os.dup2(2, 1)
     kind = CONFIGS[args.config].get("kind", "acoustic")
     if args.impl == "reference":
         # rank 0 alone runs the CPU reference; the others exit without work
         run_reference_arm(args, world, rank)
         return
     if world > 1:
-        dist_start(local)
+        with stdout_to_stderr():
+            dist_start(local)
     try:
         if kind == "diffusion":
             if rank == 0:
