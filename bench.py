@@ -622,8 +622,9 @@ def run_b200_diffusion(args, local):
                                f"launch), {launch_ms * 1e3:.2f} us per time step",
                      "alg_bytes_per_launch": 8 * pts,
                      "note": "achieved = 8 B/pt per time step over the time per step; the "
-                             "field is L2-resident, so HBM does not bind (profiles/ "
-                             "r2_c1_l2.txt has the L2 / shared-memory lens)"},
+                             "field is L2-resident, so HBM does not bind: `traffic` is the "
+                             "L2 / shared-memory lens of the kernel (ncu, profiles/"
+                             "r2_ncu_kernels.txt r2_tb_c1)"},
         "cpu_baseline": base,
         "e2e": {"value": pts * nt / e2e_s / 1e9, "unit": "GPts/s",
                 "h2d_bytes_per_step": b.u.data.nbytes, "d2h_bytes_per_step": b.u.data.nbytes},
