@@ -141,9 +141,6 @@ struct sf_plan {
     // launch geometry
     dim3 grid3;
     int zchunk = 0;
-    int64_t wpc = 0;            // balanced schedule (queue kernel), 0 = z-chunk grid
-    int tiles_x = 0, tiles = 0;
-    bool balance_disabled = false;
     int z0 = 0, z1 = 0;  // axis-0 planes the stencil updates (local coordinates)
     int tile_nx = 1, tile_ty = 8;  // 3D stencil tile: (32*tile_nx) x tile_ty
     int resident = 0;              // CTAs per SM of the chosen stencil kernel
@@ -151,7 +148,8 @@ struct sf_plan {
     bool use_tma = false;
     bool use_vec = false;  // 4 points/thread, LDS.128 variant of the TMA pipeline
     bool use_vecq = false; // ... with the a0 neighbours in a register queue (radius >= 5)
-    bool vecq_ring = false;  // ... future a0 planes from a shared-memory core ring (vecq2)
+    int vecq_ring = 0;  // ... form: 0 by radius, 1 future a0 planes from a shared-memory core ring
+                        // (vecq2), 2 compiler-scheduled addressing, 3 pinned loop state
     int vec_warps = 8;
     int vec_rpl = 1;  // vector kernel: rows of four points per lane (1 or 2)
     int tma_stages = 4;
@@ -185,8 +183,6 @@ struct sf_plan {
         int z0 = 0, z1 = 0;
         dim3 grid;
         int zchunk = 0;
-        int64_t wpc = 0;  // balanced schedule (queue kernel): plane-tiles per CTA
-        int tiles_x = 0, tiles = 0;
     };
     bool overlap = false;
     bool overlap_disabled = false;
@@ -542,10 +538,11 @@ size_t vec_smem_bytes(int r, int warps, int stages, int npme = 3, int nx = 2, in
 }
 
 template <bool FWD>
-const void* vecq_ptr(int r, int warps, bool ring = false) {
+const void* vecq_ptr(int r, int warps, int ring = 0) {
 #define SF_V(RR)                                                                               \
     case RR:                                                                                   \
-        if (ring && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq2_kernel<RR, FWD, 4>); \
+        if (ring == 1 && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq2_kernel<RR, FWD, 4>); \
+        if ((ring == 2 || (ring == 0 && RR <= 6)) && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq_free_kernel<RR, FWD, 4>); \
         return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 4>) \
                           : reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 8>);
     switch (r) {
@@ -566,12 +563,14 @@ size_t vecq_smem_bytes(int r, int warps, int stages, bool ring = false) {
 
 template <bool FWD>
 void launch_vecq(int r, int warps, dim3 g, size_t smem, cudaStream_t st, const TmaStencilArgs& A,
-                 bool ring = false) {
+                 int ring = 0) {
     const dim3 b(32 * warps);
 #define SF_V(RR)                                                                   \
     case RR:                                                                       \
-        if (ring && warps == 4)                                                    \
+        if (ring == 1 && warps == 4)                                               \
             acoustic3d_vecq2_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);            \
+        else if ((ring == 2 || (ring == 0 && RR <= 6)) && warps == 4)              \
+            acoustic3d_vecq_free_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);        \
         else if (warps == 4)                                                       \
             acoustic3d_vecq_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);             \
         else                                                                       \
@@ -738,7 +737,7 @@ void setup_tma(Plan& p) {
         }
     }
     if (p.use_vecq) {
-        const bool ring = p.vecq_ring && p.vec_warps == 4;
+        const bool ring = p.vecq_ring == 1 && p.vec_warps == 4;
         int stages = ring ? 2 : 3;  // ring: 2 stages keep 4 CTAs per SM within shared memory
         if (const char* env = std::getenv("SF_TMA_STAGES")) {
             const int v = std::atoi(env);
@@ -748,8 +747,8 @@ void setup_tma(Plan& p) {
         p.tma_stages = stages;  // <= 12: barriers + eta flags share 256 bytes
         p.tma_smem = vecq_smem_bytes(r, p.vec_warps, stages, ring);
         for (int fwd = 0; fwd < 2; ++fwd) {
-            const void* fn = fwd ? vecq_ptr<true>(r, p.vec_warps, ring)
-                                 : vecq_ptr<false>(r, p.vec_warps, ring);
+            const void* fn = fwd ? vecq_ptr<true>(r, p.vec_warps, p.vecq_ring)
+                                 : vecq_ptr<false>(r, p.vec_warps, p.vecq_ring);
             if (!fn) throw Status(SF_ERR_INVALID, "queue vector stencil not compiled");
             SF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(p.tma_smem)));
@@ -962,11 +961,6 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
         T.zchunk = zr ? zr->zchunk : p.zchunk;
         T.z0 = zr ? zr->z0 : p.z0;
         T.z1 = zr ? zr->z1 : p.z1;
-        if (p.use_vecq) {
-            T.work_per_cta = zr ? zr->wpc : p.wpc;
-            T.tiles_x = zr ? zr->tiles_x : p.tiles_x;
-            T.tiles = zr ? zr->tiles : p.tiles;
-        }
         T.stages = p.tma_stages;
         T.ce = p.ac.ce;
         T.cm = p.ac.cm;
@@ -1823,33 +1817,6 @@ void chunk_grid(const Plan& p, int64_t wx, int64_t wy, int per_sm, dim3* grid, i
                  static_cast<unsigned>((nz + zc - 1) / zc));
 }
 
-// Balanced single-wave schedule for the queue kernel: one CTA per resident
-// slot (#SM x resident CTAs/SM), each updating the same number of plane-tiles
-// of the tile-major, plane-minor order (a z-range of one or two tiles). The
-// z-chunk grid runs whole (tile, chunk) CTAs in waves: at C3 (512^3, 512
-// tiles of 64 x 8) orders 12/16 that left 14 % / 8 % of the slots idle in
-// the last wave. Falls back to the chunk grid when a CTA would get fewer
-// than 4R + 8 planes (the per-segment warm-up would dominate).
-bool balance_grid(const Plan& p, int64_t wx, int64_t wy, int per_sm, int64_t nz, dim3* grid,
-                  int64_t* wpc, int* tiles_x, int* tiles) {
-    const int r = p.ac.radius;
-    const int64_t gx = (p.n[2] + wx - 1) / wx, gy = (p.n[1] + wy - 1) / wy;
-    if (nz < 1 || per_sm < 1) return false;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device);
-    const int64_t slots = static_cast<int64_t>(sms) * per_sm;
-    const int64_t work = gx * gy * nz;
-    int64_t g = std::min<int64_t>(slots, work / (4 * r + 8));
-    if (g < 1) return false;
-    const int64_t w = (work + g - 1) / g;
-    g = (work + w - 1) / w;
-    *grid = dim3(static_cast<unsigned>(g), 1, 1);
-    *wpc = w;
-    *tiles_x = static_cast<int>(gx);
-    *tiles = static_cast<int>(gx * gy);
-    return true;
-}
-
 void set_grid(Plan& p) {
     const int r = p.ac.radius;
     const int64_t wx = p.use_vecq ? 64 : 32 * p.tile_nx;
@@ -1878,11 +1845,6 @@ void set_grid(Plan& p) {
     }
     p.resident = per_sm;
     chunk_grid(p, wx, wy, per_sm, &p.grid3, &p.zchunk);
-    p.wpc = 0;
-    if (std::getenv("SF_ZCHUNKS")) p.balance_disabled = true;  // a forced chunk count
-    if (p.use_vecq && !p.balance_disabled)
-        if (!balance_grid(p, wx, wy, per_sm, p.z1 - p.z0, &p.grid3, &p.wpc, &p.tiles_x, &p.tiles))
-            p.wpc = 0;
     if (p.slab) {
         // exchange overlap: boundary bands first, inner planes while the
         // halos are in flight (needs at least 2r owned interior planes)
@@ -1892,11 +1854,7 @@ void set_grid(Plan& p) {
             auto setr = [&](sf_plan::ZRange& z, int a, int b) {
                 z.z0 = a;
                 z.z1 = b;
-                z.wpc = 0;
                 if (b > a) chunk_grid(p, wx, wy, per_sm, &z.grid, &z.zchunk, b - a);
-                if (b > a && p.use_vecq && !p.balance_disabled)
-                    if (!balance_grid(p, wx, wy, per_sm, b - a, &z.grid, &z.wpc, &z.tiles_x, &z.tiles))
-                        z.wpc = 0;
             };
             const int lo_end = p.has_lower ? own0 + r : own0;
             const int hi_beg = p.has_upper ? own1 - r : own1;
@@ -1958,13 +1916,16 @@ void enable_tma(Plan& p) {
     if (p.ndim != 3) return;
     if (const char* env = std::getenv("SF_NO_FUSED_SPARSE")) p.fused_disabled = env[0] == '1';
     if (const char* env = std::getenv("SF_NO_ETA_SKIP")) p.eta_skip_disabled = env[0] == '1';
-    if (const char* env = std::getenv("SF_NO_BALANCE")) p.balance_disabled = env[0] == '1';
     {  // queue-vector stencil with the shared-memory core ring (vecq2), opt-in with
        // SF_VECQ2=1: 122 instead of 160 registers at radius 8 (4 CTAs per SM), but
        // the extra LDS.128 of the future planes make the LSU a second bottleneck:
        // sustained order 12 747 vs 692 us, order 16 798 vs 768 us per step
         const char* e = std::getenv("SF_VECQ2");
-        p.vecq_ring = e && e[0] == '1';
+        p.vecq_ring = e && e[0] == '1' ? 1 : 0;
+        if (const char* f = std::getenv("SF_VECQ_FORM")) {  // queue kernel form (A/B)
+            if (std::strcmp(f, "free") == 0) p.vecq_ring = 2;
+            if (std::strcmp(f, "pinned") == 0) p.vecq_ring = 3;
+        }
     }
     if (const char* env = std::getenv("SF_NO_TMA"))
         if (env[0] == '1') return;

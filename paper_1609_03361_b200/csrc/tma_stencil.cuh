@@ -50,12 +50,6 @@ struct TmaStencilArgs {
     int n0, n1, n2;
     int zchunk;
     int z0, z1;  // planes of axis 0 this launch updates
-    // balanced schedule (queue-vector kernel): 1-D grid, CTA b updates the
-    // plane-tiles [b * work_per_cta, (b + 1) * work_per_cta) of the
-    // tile-major order over tiles_x x (tiles / tiles_x) tiles; 0 = one
-    // (tile, z-chunk) per CTA on a 3-D grid
-    int64_t work_per_cta;
-    int tiles_x, tiles;
     int stages;
     float ce, cm;
     float tc[3];
