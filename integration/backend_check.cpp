@@ -5,6 +5,8 @@
 // identical copy through sf_cuda::CudaOperator on the B200, then require
 // every buffer of the two grids to be bitwise equal. Prints one JSON line per
 // case; exit status 0 when all match.
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
