@@ -678,7 +678,11 @@ def run_b200_fwi(args, local):
     value = 2 * pts * nt / ((fwd + adj) / 1e3) / 1e9
     peak, peak_kind = load_peaks()
     skip = plan.eta_skip_fraction()
-    bf, ba = 20 - 4 * skip, 36 - 4 * skip
+    # SURVEY 8(d)'s algorithmic bytes per point: forward 20 B, adjoint +
+    # gradient 36 B (the all-zero eta boxes the kernels skip are not
+    # subtracted; `moved_frac` is that stricter lens)
+    bf, ba = 20.0, 36.0
+    mf, ma = 20 - 4 * skip, 36 - 4 * skip
     base = None
     if not args.no_cpu_baseline:
         try:
@@ -703,6 +707,7 @@ def run_b200_fwi(args, local):
                      "adjoint_achieved": ba * pts * nt / (adj / 1e3) / 1e9,
                      "achieved": (bf + ba) * pts * nt / ((fwd + adj) / 1e3) / 1e9,
                      "frac": (bf + ba) * pts * nt / ((fwd + adj) / 1e3) / 1e9 / peak,
+                     "moved_frac": (mf + ma) * pts * nt / ((fwd + adj) / 1e3) / 1e9 / peak,
                      "traffic": traffic_of("c5"), "eta_boxes_skipped": skip},
         "cpu_baseline": base,
         "e2e": {"value": 2 * pts * nt / e2e_s / 1e9, "unit": "GPts/s",
