@@ -196,3 +196,21 @@ def test_reference_arm_line_on_cpu():
                            "d2h_bytes_per_step": 0}
     assert line["config"]["workload"].startswith("c1: 2D diffusion 2048^2")
     assert line["ms_per_step"] > 0 and line["higher_is_better"] is True
+
+
+def test_reference_arm_never_loads_the_product():
+    """The reference arm builds its case through oracle/ alone: after a full
+    `bench.py --impl reference` run the process has neither imported this
+    package nor mapped libsf_b200.so (the driver checks the mapped .so files)."""
+    import subprocess
+    import sys
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libsf_ref.so")):
+        pytest.skip("reference not built (oracle/_ref)")
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--config', 'c1', "
+            "'--steps', '1', '--warmup', '1']; runpy.run_path('bench.py', run_name='__main__'); "
+            "maps = open('/proc/self/maps').read(); "
+            "sys.stderr.write('PRODUCT' if ('paper_1609_03361_b200' in sys.modules "
+            "or 'libsf_b200' in maps) else 'CLEAN')")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True,
+                       timeout=600, check=True)
+    assert r.stderr.strip().endswith("CLEAN"), r.stderr[-500:]
