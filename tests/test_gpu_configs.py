@@ -18,6 +18,15 @@ field slot and trace bitwise with the checker:
   C5  301^3 order 8 FWI with 201 x 201 residual injection (40,401 injectors on
       grid nodes: colliding corners, zero weights; the grid-wide injection
       kernel path), 12 steps, vs the port's forward_history + adjoint_gradient
+
+and, through the FULL time loop against the live reference (stencilforge's own
+acoustic_build + JIT'd Operator::apply, all host threads, the medium the
+product generated handed to it):
+
+  C3  512^3 order 8, 65,536 receivers, all 500 steps
+  C4  1024^3 order 8, 8 sources, all 1000 steps (~7 min of host CPU)
+  C5  301^3 order 8 FWI through 100 steps (CPU parity at reduced
+      nt; the history of all 1000 levels, 109 GB, is GPU-only) vs the port
 """
 import gc
 
@@ -239,3 +248,81 @@ def test_c5_layout_vs_port(sf, port):
     assert_parity(v, vv, "c5 adjoint slots")
     assert_parity(srcs, s2, "c5 adjoint source traces")
     assert_parity(grad, g, "c5 gradient")
+
+
+def _full_loop_vs_reference(sf, ref, name):
+    from oracle_lib import AcousticCase, ref_acoustic
+    w = workload(sf, name)
+    s = sf.acoustic_build(model_of(sf, w), True, smooth=smooth_of(sf, w))
+    s.op.apply()
+    ref.set_threads(ref.max_threads())
+    op = ref_acoustic(ref, AcousticCase(shape=w.shape, nt=w.nt, boundary_width=w.bw,
+                                        spacing=w.h, dt=w.dt, space_order=w.order, f0=w.f0,
+                                        v_top=w.v_top, v_bottom=w.v_bottom,
+                                        src_coords=w.src_coords, rec_coords=w.rec_coords), True)
+    op.set("m", s.m.data)
+    op.set("eta", s.eta.data)
+    op.build()
+    op.apply()
+    u = op.get("u", np.float32, (3,) + w.shape)
+    assert np.abs(u).max() > 0
+    assert_parity(s.field.data, u, f"{name} slots after {w.nt} steps")
+    del u
+    assert_parity(s.rec.data.data, op.get("rec", np.float32, (w.nt, len(w.rec_coords))),
+                  f"{name} receivers")
+    # the sources and receivers the reference placed are the product's
+    assert_parity(s.src.data.data, op.get("src", np.float32, (w.nt, len(w.src_coords))),
+                  f"{name} source series")
+    del s, op
+    gc.collect()
+
+
+def test_c3o8_full_time_loop_vs_reference(sf, ref):
+    _full_loop_vs_reference(sf, ref, "c3o8")
+
+
+def test_c4_full_time_loop_vs_reference(sf, ref):
+    _full_loop_vs_reference(sf, ref, "c4")
+
+
+def test_c5_full_algorithm_reduced_nt_vs_port(sf, port):
+    """C5 as bench.py runs it (301^3, order 8, smooth medium, one source near
+    the top, 201 x 201 receivers on grid nodes, seeded N(0,1) residuals),
+    through 100 steps of forward-with-history, adjoint and gradient."""
+    import bench
+    shape, order, nt = (301, 301, 301), 8, 100
+    bw, h = bench.BW, bench.H
+    dt = min(0.4 * h / 4500.0, sf.api._stable_dt(3, order, h, 4500.0, 4500.0))
+    sm = sf.SmoothMedium(shape=shape, boundary_width=bw, spacing=h,
+                         **{k: v for k, v in bench.SMOOTH.items()})
+    lo, hi = sm.extrema()
+    m, eta = sm.generate(lo, hi)
+    mid = shape[1] // 2
+    src_c = np.array([[(bw + 2) * h, mid * h, mid * h]])
+    rec_c = np.array([[(bw + 10) * h, (bw + i) * h, (bw + j) * h]
+                      for i in range(201) for j in range(201)])
+    src_ci, src_w = port.interp(src_c, h, shape)
+    rec_ci, rec_w = port.interp(rec_c, h, shape)
+    src = np.array([port.ricker(10.0, t * dt, 0.1) for t in range(nt)], np.float32)[:, None]
+    residual = np.random.default_rng(5).standard_normal((nt, len(rec_c)), dtype=np.float32)
+    plan = sf.FwiPlan(shape, order, nt, dt, h, 1, len(rec_c))
+    rec_out, grad, v, srcs = plan.gradient(m, eta, src, src_ci, src_w, rec_ci, rec_w, residual,
+                                           want_v=True, want_src=True)
+    del plan
+    cf = port.coefs(3, order, True, dt, h)
+    hist = np.zeros((nt + 2,) + shape, np.float32)
+    rec = np.zeros((nt, len(rec_c)), np.float32)
+    port.forward_history(cf, hist, m, eta, src, src_ci, src_w, rec, rec_ci, rec_w, nt)
+    assert_parity(rec_out, rec, "c5 forward traces")
+    ca = port.coefs(3, order, False, dt, h)
+    vv = np.zeros((3,) + shape, np.float32)
+    g = np.zeros(shape, np.float32)
+    s2 = np.zeros((nt, 1), np.float32)
+    port.adjoint_gradient(ca, vv, m, eta, hist, residual, rec_ci, rec_w, s2, src_ci, src_w, g,
+                          nt)
+    del hist
+    assert np.abs(g).max() > 0
+    assert_parity(v, vv, "c5 adjoint slots")
+    assert_parity(srcs, s2, "c5 adjoint source traces")
+    assert_parity(grad, g, "c5 gradient")
+    gc.collect()
