@@ -542,6 +542,7 @@ const void* vecq_ptr(int r, int warps, int ring = 0) {
 #define SF_V(RR)                                                                               \
     case RR:                                                                                   \
         if (ring == 1 && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq2_kernel<RR, FWD, 4>); \
+        if (ring == 4) return reinterpret_cast<const void*>(&acoustic3d_vecqt_kernel<RR, FWD>);                \
         if ((ring == 2 || (ring == 0 && RR <= 6)) && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq_free_kernel<RR, FWD, 4>); \
         return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 4>) \
                           : reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 8>);
@@ -569,6 +570,8 @@ void launch_vecq(int r, int warps, dim3 g, size_t smem, cudaStream_t st, const T
     case RR:                                                                       \
         if (ring == 1 && warps == 4)                                               \
             acoustic3d_vecq2_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);            \
+        else if (ring == 4)                                                        \
+            acoustic3d_vecqt_kernel<RR, FWD><<<g, dim3(128), smem, st>>>(A);       \
         else if ((ring == 2 || (ring == 0 && RR <= 6)) && warps == 4)              \
             acoustic3d_vecq_free_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);        \
         else if (warps == 4)                                                       \
@@ -746,6 +749,13 @@ void setup_tma(Plan& p) {
         if (p.stages_override >= 2) stages = std::min(p.stages_override, 12);
         p.tma_stages = stages;  // <= 12: barriers + eta flags share 256 bytes
         p.tma_smem = vecq_smem_bytes(r, p.vec_warps, stages, ring);
+        if (p.vecq_ring == 4) {
+            // TMEM queue: 128 columns per CTA, so at most 4 CTAs per SM may be
+            // resident (a fifth would wait in tcgen05.alloc): shared memory
+            // sized to allow no more than 4
+            p.vec_warps = 4;
+            p.tma_smem = std::max<size_t>(p.tma_smem, 228 * 1024 / 5 + 1024);
+        }
         for (int fwd = 0; fwd < 2; ++fwd) {
             const void* fn = fwd ? vecq_ptr<true>(r, p.vec_warps, p.vecq_ring)
                                  : vecq_ptr<false>(r, p.vec_warps, p.vecq_ring);
@@ -1925,6 +1935,7 @@ void enable_tma(Plan& p) {
         if (const char* f = std::getenv("SF_VECQ_FORM")) {  // queue kernel form (A/B)
             if (std::strcmp(f, "free") == 0) p.vecq_ring = 2;
             if (std::strcmp(f, "pinned") == 0) p.vecq_ring = 3;
+            if (std::strcmp(f, "tmem") == 0) p.vecq_ring = 4;
         }
     }
     if (const char* env = std::getenv("SF_NO_TMA"))

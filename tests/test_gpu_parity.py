@@ -338,7 +338,7 @@ VARIANTS = [{}, {"SF_VEC": "0"}, {"SF_NO_TMA": "1"}, {"SF_VEC": "0", "SF_TMA": "
             {"SF_VEC_RPL": "2"}, {"SF_VEC_RPL": "2", "SF_VEC_NX": "1"},
             {"SF_VEC_RPL": "2", "SF_VEC_NX": "2", "SF_VEC_WARPS": "8"}, {"SF_VECQ2": "1"},
             {"SF_VECQ2": "1", "SF_TMA_STAGES": "3"}, {"SF_VECQ_FORM": "free"},
-            {"SF_VECQ_FORM": "pinned"}]
+            {"SF_VECQ_FORM": "pinned"}, {"SF_VECQ_FORM": "tmem"}]
 
 
 @pytest.mark.parametrize("order", [2, 6, 8, 12, 16])
@@ -366,11 +366,16 @@ def test_every_kernel_variant_bitwise(sf, port, monkeypatch, order, env):
 
 @pytest.mark.parametrize("order", [10, 12, 14, 16])
 @pytest.mark.parametrize("zchunks", ["1", "3"])
-def test_queue_kernel_long_chunks(sf, port, monkeypatch, order, zchunks):
+@pytest.mark.parametrize("form", ["default", "tmem"])
+def test_queue_kernel_long_chunks(sf, port, monkeypatch, order, zchunks, form):
     """The queue-vector kernel over a-0 chunks long enough for every pipeline
     stage to be refilled many times and the register queue to cycle through
-    many two-step passes, odd and even chunk lengths: bitwise the oracle."""
+    many two-step passes (or, in the TMEM form, the window to be moved back
+    to slot 0 several times), odd and even chunk lengths: bitwise the
+    oracle."""
     monkeypatch.setenv("SF_ZCHUNKS", zchunks)
+    if form != "default":
+        monkeypatch.setenv("SF_VECQ_FORM", form)
     shape = (97, 30, 77)
     nt = 4
     c = random_case(port, shape, order, seed=order + 7)
