@@ -512,6 +512,8 @@ const void* vec_ptr_r(int warps, int nx, int rpl) {
     if (nx == 1)
         return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4, false, 8>)
                           : nullptr;
+    if (warps == 16)  // 64 x 32 tiles, one CTA per SM (radius 4 only)
+        return RR == 4 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<4, FWD, 16>) : nullptr;
     return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4>)
                       : reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 8>);
 }
@@ -649,6 +651,8 @@ void launch_vec(int r, int warps, int nx, int rpl, dim3 g, size_t smem, cudaStre
             launch_pdl(acoustic3d_vec_kernel<RR, FWD, 4, false, 8>, g, b, smem, st, A);      \
         else if (warps == 4)                                                                 \
             launch_pdl(acoustic3d_vec_kernel<RR, FWD, 4>, g, b, smem, st, A);                \
+        else if (warps == 16)                                                                \
+            launch_pdl(acoustic3d_vec_kernel<4, FWD, 16>, g, b, smem, st, A);                \
         else                                                                                 \
             launch_pdl(acoustic3d_vec_kernel<RR, FWD, 8>, g, b, smem, st, A);                \
         return;
@@ -768,7 +772,8 @@ void setup_tma(Plan& p) {
     if (p.use_vec) {
         int stages = 3;
         const int rpl = p.vec_rpl;
-        while (stages > 2 && vec_smem_bytes(r, p.vec_warps, stages, 3, nx, rpl) * 2 > 226 * 1024)
+        const size_t ctas = p.vec_warps == 16 ? 1 : 2;  // CTAs per SM the depth must leave room for
+        while (stages > 2 && vec_smem_bytes(r, p.vec_warps, stages, 3, nx, rpl) * ctas > 226 * 1024)
             --stages;
         if (const char* env = std::getenv("SF_TMA_STAGES")) {
             const int v = std::atoi(env);
@@ -1948,7 +1953,20 @@ void enable_tma(Plan& p) {
         // FWI: the forward runs the same tile choice as a plain forward plan;
         // the 4-warp gradient kernel has its own maps (setup_tma)
         p.vec_warps = p.ac.radius <= 3 ? 4 : 8;
-        if (const char* w = std::getenv("SF_VEC_WARPS")) p.vec_warps = std::atoi(w) == 4 ? 4 : 8;
+        if (p.ac.radius == 4 && p.kind != Plan::FWI) {
+            // 64 x 32 tiles (16 consumer warps, one CTA per SM): the cur box
+            // carries 1.41x instead of 1.69x its points, so less L2 and
+            // shared-memory traffic per point -- C4 3878 vs 3966 us, C3
+            // order 8 502 vs 508 us per step (interleaved A/B) -- where the
+            // taller tiles do not pad the a1 extent by more than ~3 %
+            const int64_t n1 = p.n[1] - 4;
+            const int64_t pad16 = (n1 + 15) / 16 * 16, pad32 = (n1 + 31) / 32 * 32;
+            if (pad32 * 100 <= pad16 * 103) p.vec_warps = 16;
+        }
+        if (const char* w = std::getenv("SF_VEC_WARPS")) {
+            const int v = std::atoi(w);
+            p.vec_warps = v == 4 ? 4 : v == 16 && p.ac.radius == 4 ? 16 : 8;
+        }
         // tile width: 64 (16 lanes per row) unless 32-wide 4-warp tiles
         // cover the interior with fewer padded points (FWI: 64 wide, one set
         // of maps serves the forward and gradient kernels)

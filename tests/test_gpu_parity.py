@@ -338,7 +338,7 @@ VARIANTS = [{}, {"SF_VEC": "0"}, {"SF_NO_TMA": "1"}, {"SF_VEC": "0", "SF_TMA": "
             {"SF_VEC_RPL": "2"}, {"SF_VEC_RPL": "2", "SF_VEC_NX": "1"},
             {"SF_VEC_RPL": "2", "SF_VEC_NX": "2", "SF_VEC_WARPS": "8"}, {"SF_VECQ2": "1"},
             {"SF_VECQ2": "1", "SF_TMA_STAGES": "3"}, {"SF_VECQ_FORM": "free"},
-            {"SF_VECQ_FORM": "pinned"}, {"SF_VECQ_FORM": "tmem"}]
+            {"SF_VECQ_FORM": "pinned"}, {"SF_VECQ_FORM": "tmem"}, {"SF_VEC_WARPS": "16"}]
 
 
 @pytest.mark.parametrize("order", [2, 6, 8, 12, 16])
