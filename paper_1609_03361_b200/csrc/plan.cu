@@ -499,7 +499,8 @@ size_t tma_smem_bytes(int r, int nx, int stages) {
 // ---- vectorised TMA path (4 consecutive a2 points per thread) -------------
 // tile_nx selects the tile width for the vector kernel: 2 -> 64-wide tiles
 // (16 lanes per row), 1 -> 32-wide (8 lanes per row); rpl = rows per lane.
-// Compiled shapes (warps, nx, rpl): (4,2,1) (8,2,1) (4,1,1) (2,1,2) (4,2,2).
+// Compiled shapes (warps, nx, rpl): (4,2,1) (8,2,1) (4,1,1) (8,1,1) (2,1,2) (4,2,2), and
+// (16,2,1) at radius 4.
 template <bool FWD, int RR>
 const void* vec_ptr_r(int warps, int nx, int rpl) {
     if (rpl == 2) {
@@ -510,8 +511,9 @@ const void* vec_ptr_r(int warps, int nx, int rpl) {
         return nullptr;
     }
     if (nx == 1)
-        return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4, false, 8>)
-                          : nullptr;
+        return warps == 4   ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4, false, 8>)
+               : warps == 8 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 8, false, 8>)
+                            : nullptr;
     if (warps == 16)  // 64 x 32 tiles, one CTA per SM (radius 4 only)
         return RR == 4 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<4, FWD, 16>) : nullptr;
     return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4>)
@@ -647,6 +649,8 @@ void launch_vec(int r, int warps, int nx, int rpl, dim3 g, size_t smem, cudaStre
             launch_pdl(acoustic3d_vec_kernel<RR, FWD, 2, false, 8, 2>, g, b, smem, st, A);   \
         else if (rpl == 2)                                                                   \
             launch_pdl(acoustic3d_vec_kernel<RR, FWD, 4, false, 16, 2>, g, b, smem, st, A);  \
+        else if (nx == 1 && warps == 8)                                                      \
+            launch_pdl(acoustic3d_vec_kernel<RR, FWD, 8, false, 8>, g, b, smem, st, A);      \
         else if (nx == 1)                                                                    \
             launch_pdl(acoustic3d_vec_kernel<RR, FWD, 4, false, 8>, g, b, smem, st, A);      \
         else if (warps == 4)                                                                 \
@@ -1983,7 +1987,10 @@ void enable_tma(Plan& p) {
             }
             if (const char* e = std::getenv("SF_VEC_NX")) {
                 p.tile_nx = std::atoi(e) == 1 ? 1 : 2;
-                if (p.tile_nx == 1) p.vec_warps = 4;
+                if (p.tile_nx == 1) {  // 32-wide tiles: 32 x 16 (4 warps) or 32 x 32 (8 warps)
+                    const char* w = std::getenv("SF_VEC_WARPS");
+                    p.vec_warps = w && std::atoi(w) == 8 ? 8 : 4;
+                }
             }
             // two rows per lane: same tile, half the consumer warps
             p.vec_rpl = 1;

@@ -255,7 +255,10 @@ def test_diffusion_config1_layout_and_oracle(sf, port):
     assert_parity(b.u.data, u)
 
 
-def test_fwi_gradient_vs_oracle(sf, port):
+@pytest.mark.parametrize("warps", ["default", "16"])
+def test_fwi_gradient_vs_oracle(sf, port, monkeypatch, warps):
+    if warps != "default":  # forward sweep on 64 x 32 tiles
+        monkeypatch.setenv("SF_VEC_WARPS", warps)
     shape = (34, 30, 40)
     order, nt = 8, 25
     c = random_case(port, shape, order, seed=5, nsrc=1, nrec=40)
@@ -338,7 +341,8 @@ VARIANTS = [{}, {"SF_VEC": "0"}, {"SF_NO_TMA": "1"}, {"SF_VEC": "0", "SF_TMA": "
             {"SF_VEC_RPL": "2"}, {"SF_VEC_RPL": "2", "SF_VEC_NX": "1"},
             {"SF_VEC_RPL": "2", "SF_VEC_NX": "2", "SF_VEC_WARPS": "8"}, {"SF_VECQ2": "1"},
             {"SF_VECQ2": "1", "SF_TMA_STAGES": "3"}, {"SF_VECQ_FORM": "free"},
-            {"SF_VECQ_FORM": "pinned"}, {"SF_VECQ_FORM": "tmem"}, {"SF_VEC_WARPS": "16"}]
+            {"SF_VECQ_FORM": "pinned"}, {"SF_VECQ_FORM": "tmem"}, {"SF_VEC_WARPS": "16"},
+            {"SF_VEC_NX": "1", "SF_VEC_WARPS": "8"}]
 
 
 @pytest.mark.parametrize("order", [2, 6, 8, 12, 16])
