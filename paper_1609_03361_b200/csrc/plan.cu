@@ -2302,6 +2302,9 @@ std::vector<StencilConfig> tune_candidates(const Plan& p) {
         for (int st : {2, 3, 4}) out.push_back({2, 1, 16, 4, st});
         for (int st : {2, 3, 4}) out.push_back({2, 1, 16, 2, st});  // 2 rows per lane
         for (int st : {2, 3}) out.push_back({2, 2, 16, 4, st});     // 2 rows per lane
+        for (int st : {2, 3}) out.push_back({2, 1, 32, 8, st});     // 32 x 32 tiles
+        if (r == 4)
+            for (int st : {2, 3}) out.push_back({2, 2, 32, 16, st});  // 64 x 32, one CTA per SM
     }
     if (r >= 5)
         for (int w : {4, 8})
