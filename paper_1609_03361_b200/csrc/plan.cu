@@ -2641,8 +2641,9 @@ extern "C" int sf_selftest_reciprocal(int device, unsigned long long* mismatches
         unsigned long long* d = dalloc<unsigned long long>(1);
         SF_CUDA(cudaMemset(d, 0, sizeof(unsigned long long)));
         const uint32_t chunk = 1u << 30;  // float bit patterns per launch
-        for (uint64_t first = 0; first < (1ull << 32); first += chunk)
-            rcp4_check_kernel<<<chunk / 4 / 256, 256>>>(static_cast<uint32_t>(first), chunk, d);
+        for (int mode = 0; mode < 2; ++mode)
+            for (uint64_t first = 0; first < (1ull << 32); first += chunk)
+                rcp4_check_kernel<<<chunk / 4 / 256, 256>>>(static_cast<uint32_t>(first), chunk, mode, d);
         SF_CUDA(cudaGetLastError());
         SF_CUDA(cudaMemcpy(mismatches, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
         dfree(d);
