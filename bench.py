@@ -56,7 +56,7 @@ CONFIGS = {
     "c2": dict(shape=(281, 281, 281), order=4, nt=625, layered=True),
     # SURVEY C3 / BASELINE configs[2] (one order per run), 256 x 256 receivers
     **{f"c3o{o}": dict(shape=(512, 512, 512), order=o, nt=500, recs="surface")
-       for o in (4, 6, 8, 12, 16)},
+       for o in (4, 6, 8, 10, 12, 14, 16)},
 }
 BW, H = 40, 10.0
 

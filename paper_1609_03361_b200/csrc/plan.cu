@@ -40,6 +40,7 @@
 
 #include "../../include/sf_b200.h"
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges are no-ops unless a profiler injects NVTX
 
 #include "kernels.cuh"
 #include "tma_stencil.cuh"
@@ -49,6 +50,15 @@
 #include "medium.h"
 
 namespace sfb {
+
+// NVTX range over a phase of a C-ABI call (upload / time loop / download /
+// FWI sweeps / autotune / slab chain); shows up in Nsight Systems timelines.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 namespace {
 thread_local std::string g_error;
@@ -152,6 +162,8 @@ struct sf_plan {
                         // (vecq2), 2 compiler-scheduled addressing, 3 pinned loop state
     int vec_warps = 8;
     int vec_rpl = 1;  // vector kernel: rows of four points per lane (1 or 2)
+    bool vec_aq = true;  // 16-warp radius-4 ring kernel with the a0 register queue (SF_VEC_AQ=0: ring loads)
+    int vec_kernel_rpl() const { return vec_aq && vec_warps == 16 && vec_rpl == 1 ? 17 : vec_rpl; }
     int tma_stages = 4;
     int stages_override = 0;  // autotune: > 0 forces the pipeline depth
     size_t tma_smem = 0;
@@ -501,6 +513,10 @@ size_t tma_smem_bytes(int r, int nx, int stages) {
 // (16 lanes per row), 1 -> 32-wide (8 lanes per row); rpl = rows per lane.
 // Compiled shapes (warps, nx, rpl): (4,2,1) (8,2,1) (4,1,1) (8,1,1) (2,1,2) (4,2,2), and
 // (16,2,1) at radius 4.
+// rows-per-lane code of the 16-warp radius-4 kernel with the a0 register
+// queue (one row per lane; geometry as rpl = 1)
+constexpr int kRplAq = 17;
+
 template <bool FWD, int RR>
 const void* vec_ptr_r(int warps, int nx, int rpl) {
     if (rpl == 2) {
@@ -514,6 +530,10 @@ const void* vec_ptr_r(int warps, int nx, int rpl) {
         return warps == 4   ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4, false, 8>)
                : warps == 8 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 8, false, 8>)
                             : nullptr;
+    if (warps == 16 && rpl == kRplAq)  // the same with the a0 register queue (SF_VEC_AQ=1)
+        return RR == 4 ? reinterpret_cast<const void*>(
+                             &acoustic3d_vec_kernel<4, FWD, 16, false, 16, 1, true>)
+                       : nullptr;
     if (warps == 16)  // 64 x 32 tiles, one CTA per SM (radius 4 only)
         return RR == 4 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<4, FWD, 16>) : nullptr;
     return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4>)
@@ -547,7 +567,8 @@ const void* vecq_ptr(int r, int warps, int ring = 0) {
     case RR:                                                                                   \
         if (ring == 1 && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq2_kernel<RR, FWD, 4>); \
         if (ring == 4) return reinterpret_cast<const void*>(&acoustic3d_vecqt_kernel<RR, FWD>);                \
-        if ((ring == 2 || (ring == 0 && RR <= 6)) && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq_free_kernel<RR, FWD, 4>); \
+        if ((ring == 5 || (ring == 0 && RR == 6)) && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 4, true>); \
+        if (ring == 2 && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq_free_kernel<RR, FWD, 4>); \
         return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 4>) \
                           : reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 8>);
     switch (r) {
@@ -576,7 +597,9 @@ void launch_vecq(int r, int warps, dim3 g, size_t smem, cudaStream_t st, const T
             acoustic3d_vecq2_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);            \
         else if (ring == 4)                                                        \
             acoustic3d_vecqt_kernel<RR, FWD><<<g, dim3(128), smem, st>>>(A);       \
-        else if ((ring == 2 || (ring == 0 && RR <= 6)) && warps == 4)              \
+        else if ((ring == 5 || (ring == 0 && RR == 6)) && warps == 4)              \
+            acoustic3d_vecq_kernel<RR, FWD, 4, true><<<g, b, smem, st>>>(A);       \
+        else if (ring == 2 && warps == 4)                                          \
             acoustic3d_vecq_free_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);        \
         else if (warps == 4)                                                       \
             acoustic3d_vecq_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);             \
@@ -645,7 +668,9 @@ void launch_vec(int r, int warps, int nx, int rpl, dim3 g, size_t smem, cudaStre
     const dim3 b(32 * (warps + 1));  // + the TMA producer warp
 #define SF_V(RR)                                                                             \
     case RR:                                                                                 \
-        if (rpl == 2 && nx == 1)                                                             \
+        if (rpl == kRplAq)                                                                   \
+            launch_pdl(acoustic3d_vec_kernel<4, FWD, 16, false, 16, 1, true>, g, b, smem, st, A); \
+        else if (rpl == 2 && nx == 1)                                                        \
             launch_pdl(acoustic3d_vec_kernel<RR, FWD, 2, false, 8, 2>, g, b, smem, st, A);   \
         else if (rpl == 2)                                                                   \
             launch_pdl(acoustic3d_vec_kernel<RR, FWD, 4, false, 16, 2>, g, b, smem, st, A);  \
@@ -787,8 +812,8 @@ void setup_tma(Plan& p) {
         p.tma_stages = stages;  // <= 12: barriers + eta flags share 256 bytes
         p.tma_smem = vec_smem_bytes(r, p.vec_warps, stages, 3, nx, rpl);
         for (int fwd = 0; fwd < 2; ++fwd) {
-            const void* fn = fwd ? vec_ptr<true>(r, p.vec_warps, nx, rpl)
-                                 : vec_ptr<false>(r, p.vec_warps, nx, rpl);
+            const void* fn = fwd ? vec_ptr<true>(r, p.vec_warps, nx, p.vec_kernel_rpl())
+                                 : vec_ptr<false>(r, p.vec_warps, nx, p.vec_kernel_rpl());
             if (!fn) throw Status(SF_ERR_INVALID, "vector stencil not compiled");
             SF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(p.tma_smem)));
@@ -1059,11 +1084,11 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
                 T.smp_np = static_cast<int>(epi->smp->np);
             }
             if (p.ac.forward)
-                launch_vec<true>(p.ac.radius, p.vec_warps, p.tile_nx, p.vec_rpl, grid3, p.tma_smem,
-                                 p.stream, T);
+                launch_vec<true>(p.ac.radius, p.vec_warps, p.tile_nx, p.vec_kernel_rpl(), grid3,
+                                 p.tma_smem, p.stream, T);
             else
-                launch_vec<false>(p.ac.radius, p.vec_warps, p.tile_nx, p.vec_rpl, grid3, p.tma_smem,
-                                  p.stream, T);
+                launch_vec<false>(p.ac.radius, p.vec_warps, p.tile_nx, p.vec_kernel_rpl(), grid3,
+                                  p.tma_smem, p.stream, T);
             return;
         }
         if (p.ac.forward)
@@ -1777,6 +1802,7 @@ void run_steps(Plan& p, int64_t b, int64_t e) {
     auto key = std::make_pair(b, e);
     auto it = p.graphs.find(key);
     if (it == p.graphs.end()) {
+        NvtxRange cap("capture time loop into a CUDA graph");
         cudaGraph_t g = nullptr;
         SF_CUDA(cudaStreamBeginCapture(p.stream, cudaStreamCaptureModeThreadLocal));
         try {
@@ -1849,8 +1875,8 @@ void set_grid(Plan& p) {
         if (fn)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * p.vec_warps, p.tma_smem);
     } else if (p.use_vec) {
-        const void* fn = p.ac.forward ? vec_ptr<true>(r, p.vec_warps, p.tile_nx, p.vec_rpl)
-                                      : vec_ptr<false>(r, p.vec_warps, p.tile_nx, p.vec_rpl);
+        const void* fn = p.ac.forward ? vec_ptr<true>(r, p.vec_warps, p.tile_nx, p.vec_kernel_rpl())
+                                      : vec_ptr<false>(r, p.vec_warps, p.tile_nx, p.vec_kernel_rpl());
         if (fn)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * (p.vec_warps + 1),
                                                           p.tma_smem);
@@ -1945,6 +1971,7 @@ void enable_tma(Plan& p) {
             if (std::strcmp(f, "free") == 0) p.vecq_ring = 2;
             if (std::strcmp(f, "pinned") == 0) p.vecq_ring = 3;
             if (std::strcmp(f, "tmem") == 0) p.vecq_ring = 4;
+            if (std::strcmp(f, "last") == 0) p.vecq_ring = 5;  // decoupled, last warp out refills
         }
     }
     if (const char* env = std::getenv("SF_NO_TMA"))
@@ -1992,6 +2019,7 @@ void enable_tma(Plan& p) {
                     p.vec_warps = w && std::atoi(w) == 8 ? 8 : 4;
                 }
             }
+            if (const char* e = std::getenv("SF_VEC_AQ")) p.vec_aq = std::atoi(e) != 0;
             // two rows per lane: same tile, half the consumer warps
             p.vec_rpl = 1;
             if (const char* e = std::getenv("SF_VEC_RPL"))
@@ -2325,6 +2353,7 @@ extern "C" int sf_plan_autotune(sf_plan* p, int64_t tune_steps, int repeats, sf_
             throw Status(SF_ERR_INVALID, "autotune tunes single-domain 3D acoustic plans");
         if (tune_steps < 1 || tune_steps > p->nt) throw Status(SF_ERR_INVALID, "tune_steps range");
         if (repeats < 1) repeats = 1;
+        NvtxRange nvtx("sf_plan_autotune");
         SF_CUDA(cudaSetDevice(p->device));
         // snapshot what a run modifies: the three slots and both series
         const size_t fbytes = sizeof(float) * (p->slot_elems + field_slack(*p));
@@ -2843,6 +2872,7 @@ int sf_slab_chain_run(sf_plan* const* plans, int nplans, int64_t b, int64_t e) {
             // overlap the flags kernel, so finish it here
             SF_CUDA(cudaStreamSynchronize(plans[i]->stream));
         }
+        sfb::NvtxRange r("sf_slab_chain_run: time loop");
         for (int64_t k = b; k < e; ++k) sfb::chain_step(plans, nplans, k);
         for (int i = 0; i < nplans; ++i) sfb::check_kernel_errors(*plans[i]);
     });
@@ -2889,12 +2919,18 @@ int64_t sf_plan_arg_bytes(const sf_plan* p, int i) {
 
 int sf_plan_upload(sf_plan* p, void* const* args, int nargs) {
     if (!p) return SF_ERR_INVALID;
-    return guard([&] { sfb::upload_any(*p, args, nargs); });
+    return guard([&] {
+        sfb::NvtxRange r("sf_plan_upload");
+        sfb::upload_any(*p, args, nargs);
+    });
 }
 
 int sf_plan_download(sf_plan* p, void* const* args, int nargs) {
     if (!p) return SF_ERR_INVALID;
-    return guard([&] { sfb::download_any(*p, args, nargs); });
+    return guard([&] {
+        sfb::NvtxRange r("sf_plan_download");
+        sfb::download_any(*p, args, nargs);
+    });
 }
 
 int sf_plan_run(sf_plan* p, int64_t b, int64_t e) {
@@ -2903,6 +2939,7 @@ int sf_plan_run(sf_plan* p, int64_t b, int64_t e) {
         if (p->kind == sf_plan::FWI) throw Status(SF_ERR_INVALID, "use sf_fwi_gradient");
         if (b < 0 || e > p->nt || b > e) throw Status(SF_ERR_INVALID, "step range out of bounds");
         SF_CUDA(cudaSetDevice(p->device));
+        sfb::NvtxRange r("sf_plan_run: time loop");
         sfb::run_steps(*p, b, e);
         SF_CUDA(cudaGetLastError());
     });
@@ -2919,9 +2956,17 @@ int sf_plan_invoke(sf_plan* p, void* const* args, int nargs) {
         if (p->kind == sf_plan::FWI) throw Status(SF_ERR_INVALID, "use sf_fwi_gradient");
         for (int i = 0; i < nargs; ++i)
             if (!args[i]) throw Status(SF_ERR_SIGNATURE, "null buffer for " + p->arg_names.at(i));
-        sfb::upload_any(*p, args, nargs);
-        sfb::run_steps(*p, 0, p->nt);
-        sfb::check_kernel_errors(*p);
+        sfb::NvtxRange whole("sf_plan_invoke");
+        {
+            sfb::NvtxRange r("upload (H2D + repack)");
+            sfb::upload_any(*p, args, nargs);
+        }
+        {
+            sfb::NvtxRange r("time loop");
+            sfb::run_steps(*p, 0, p->nt);
+            sfb::check_kernel_errors(*p);
+        }
+        sfb::NvtxRange r("download (repack + D2H)");
         // only what the kernel writes comes back (the generated Operator
         // stores into the field and the sampled series; m, eta, the injected
         // series, ci and w are read-only, so the host copies already match)
@@ -3015,14 +3060,18 @@ int sf_fwi_gradient(sf_plan* p, const float* m, const float* eta, const float* s
         if (!m || !eta || !src || !src_ci || !src_w || !rec_ci || !rec_w || !residual)
             throw Status(SF_ERR_SIGNATURE, "null input buffer");
         SF_CUDA(cudaSetDevice(p->device));
+        sfb::NvtxRange whole("sf_fwi_gradient");
         sfb::h2d_field(*p, p->m, m);
         sfb::h2d_field(*p, p->eta, eta);
         ++p->eta_gen;
         // forward: src injects, rec samples
         sfb::upload_points(*p, p->src, src, src_ci, src_w, true);
         sfb::upload_points(*p, p->rec, nullptr, rec_ci, rec_w, true);
-        sfb::run_steps(*p, sfb::kFwiForward, sfb::kFwiForward);
-        sfb::check_kernel_errors(*p);
+        {
+            sfb::NvtxRange r("FWI forward sweep (history)");
+            sfb::run_steps(*p, sfb::kFwiForward, sfb::kFwiForward);
+            sfb::check_kernel_errors(*p);
+        }
         if (rec_out)
             SF_CUDA(cudaMemcpyAsync(rec_out, p->rec.series, sizeof(float) * p->nt * p->rec.np,
                                     cudaMemcpyDeviceToHost, p->stream));
@@ -3030,8 +3079,11 @@ int sf_fwi_gradient(sf_plan* p, const float* m, const float* eta, const float* s
         SF_CUDA(cudaStreamSynchronize(p->stream));
         SF_CUDA(cudaMemcpyAsync(p->rec.series, residual, sizeof(float) * p->nt * p->rec.np,
                                 cudaMemcpyHostToDevice, p->stream));
-        sfb::run_steps(*p, sfb::kFwiAdjoint, sfb::kFwiAdjoint);
-        sfb::check_kernel_errors(*p);
+        {
+            sfb::NvtxRange r("FWI adjoint + gradient sweep");
+            sfb::run_steps(*p, sfb::kFwiAdjoint, sfb::kFwiAdjoint);
+            sfb::check_kernel_errors(*p);
+        }
         if (grad_out) sfb::d2h_field(*p, grad_out, p->grad);
         if (v_out)
             for (int s = 0; s < 3; ++s)

@@ -342,7 +342,8 @@ VARIANTS = [{}, {"SF_VEC": "0"}, {"SF_NO_TMA": "1"}, {"SF_VEC": "0", "SF_TMA": "
             {"SF_VEC_RPL": "2", "SF_VEC_NX": "2", "SF_VEC_WARPS": "8"}, {"SF_VECQ2": "1"},
             {"SF_VECQ2": "1", "SF_TMA_STAGES": "3"}, {"SF_VECQ_FORM": "free"},
             {"SF_VECQ_FORM": "pinned"}, {"SF_VECQ_FORM": "tmem"}, {"SF_VEC_WARPS": "16"},
-            {"SF_VEC_NX": "1", "SF_VEC_WARPS": "8"}]
+            {"SF_VEC_NX": "1", "SF_VEC_WARPS": "8"}, {"SF_VEC_WARPS": "16", "SF_VEC_AQ": "1"}, {"SF_VEC_WARPS": "16", "SF_VEC_AQ": "0"},
+            {"SF_VECQ_FORM": "last"}]
 
 
 @pytest.mark.parametrize("order", [2, 6, 8, 12, 16])
@@ -370,7 +371,7 @@ def test_every_kernel_variant_bitwise(sf, port, monkeypatch, order, env):
 
 @pytest.mark.parametrize("order", [10, 12, 14, 16])
 @pytest.mark.parametrize("zchunks", ["1", "3"])
-@pytest.mark.parametrize("form", ["default", "tmem"])
+@pytest.mark.parametrize("form", ["default", "tmem", "last"])
 def test_queue_kernel_long_chunks(sf, port, monkeypatch, order, zchunks, form):
     """The queue-vector kernel over a-0 chunks long enough for every pipeline
     stage to be refilled many times and the register queue to cycle through
