@@ -568,6 +568,9 @@ const void* vecq_ptr(int r, int warps, int ring = 0) {
         if (ring == 1 && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq2_kernel<RR, FWD, 4>); \
         if (ring == 4) return reinterpret_cast<const void*>(&acoustic3d_vecqt_kernel<RR, FWD>);                \
         if ((ring == 5 || (ring == 0 && RR == 6)) && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 4, true>); \
+        if (ring == 5 && warps == 8) return reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 8, true>); \
+        if (warps == 12) return RR >= 7 ? (ring == 5 ? reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<(RR >= 7 ? RR : 7), FWD, 12, true>) \
+                                                     : reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<(RR >= 7 ? RR : 7), FWD, 12>)) : nullptr; \
         if (ring == 2 && warps == 4) return reinterpret_cast<const void*>(&acoustic3d_vecq_free_kernel<RR, FWD, 4>); \
         return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 4>) \
                           : reinterpret_cast<const void*>(&acoustic3d_vecq_kernel<RR, FWD, 8>);
@@ -599,6 +602,12 @@ void launch_vecq(int r, int warps, dim3 g, size_t smem, cudaStream_t st, const T
             acoustic3d_vecqt_kernel<RR, FWD><<<g, dim3(128), smem, st>>>(A);       \
         else if ((ring == 5 || (ring == 0 && RR == 6)) && warps == 4)              \
             acoustic3d_vecq_kernel<RR, FWD, 4, true><<<g, b, smem, st>>>(A);       \
+        else if (ring == 5 && warps == 8)                                          \
+            acoustic3d_vecq_kernel<RR, FWD, 8, true><<<g, b, smem, st>>>(A);       \
+        else if (warps == 12 && RR >= 7 && ring == 5)                              \
+            acoustic3d_vecq_kernel<(RR >= 7 ? RR : 7), FWD, 12, true><<<g, b, smem, st>>>(A); \
+        else if (warps == 12 && RR >= 7)                                           \
+            acoustic3d_vecq_kernel<(RR >= 7 ? RR : 7), FWD, 12><<<g, b, smem, st>>>(A); \
         else if (ring == 2 && warps == 4)                                          \
             acoustic3d_vecq_free_kernel<RR, FWD, 4><<<g, b, smem, st>>>(A);        \
         else if (warps == 4)                                                       \
@@ -2037,7 +2046,10 @@ void enable_tma(Plan& p) {
         p.use_vec = true;
         p.use_vecq = true;
         p.vec_warps = 4;
-        if (const char* w = std::getenv("SF_VEC_WARPS")) p.vec_warps = std::atoi(w) == 8 ? 8 : 4;
+        if (const char* w = std::getenv("SF_VEC_WARPS")) {
+            const int v = std::atoi(w);
+            p.vec_warps = v == 8 ? 8 : (v == 12 && p.ac.radius >= 7) ? 12 : 4;  // 64 x 8 / 16 / 24 tiles
+        }
         setup_tma(p);
         p.use_tma = true;
         set_grid(p);
