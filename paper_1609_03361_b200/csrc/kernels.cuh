@@ -279,12 +279,20 @@ struct InjectArgs {
     const float* cw;          // contribution weight w[p][k]
     float scale;
     int ncells;
+    // plane filter (time-skewed steps, plan.cu invoke_overlapped): when
+    // zf1 > 0 only cells whose a0 plane lies in [zf0, zf1) are injected
+    int64_t plane;
+    int zf0, zf1;
 };
 
 __global__ void __launch_bounds__(256) inject_kernel(const InjectArgs A) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= A.ncells) return;
     const int64_t off = A.cell_off[i];
+    if (A.zf1 > 0) {
+        const int z = static_cast<int>(off / A.plane);
+        if (z < A.zf0 || z >= A.zf1) return;
+    }
     float v = A.field[off];
     const float mv = __ldg(A.m + off);
     for (int j = A.start[i]; j < A.start[i + 1]; ++j) {
@@ -304,6 +312,9 @@ struct SampleArgs {
     float* out;        // series row of this step
     int64_t pitch, plane;
     int np;
+    // plane filter (time-skewed steps): when zf1 > 0 only points whose upper
+    // corner plane c0 + 1 lies in [zf0, zf1) are sampled
+    int zf0, zf1;
 };
 
 template <int NDIM>
@@ -314,6 +325,7 @@ __global__ void __launch_bounds__(256) sample_kernel(const SampleArgs A) {
     const int c0 = A.ci[p * NDIM + 0];
     const int c1 = A.ci[p * NDIM + 1];
     const int c2 = NDIM == 3 ? A.ci[p * NDIM + 2] : 0;
+    if (A.zf1 > 0 && (c0 + 1 < A.zf0 || c0 + 1 >= A.zf1)) return;
     float acc = 0.0f;
 #pragma unroll
     for (int k = 0; k < C; ++k) {

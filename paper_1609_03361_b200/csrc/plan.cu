@@ -180,6 +180,10 @@ struct sf_plan {
     std::vector<std::string> arg_names;
     std::vector<int64_t> arg_bytes;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // sf_plan_invoke with the upload overlapped by the first time steps
+    // (invoke_overlapped): the copy stream and one event per plane chunk
+    cudaStream_t io = nullptr;
+    std::vector<cudaEvent_t> ev_up;
     int64_t launches_per_step = 0;
     // depth-slab decomposition; a whole grid is one slab
     bool slab = false;
@@ -656,6 +660,12 @@ bool pdl_enabled() {
     return on;
 }
 
+// Set while the time-skewed steps of invoke_overlapped are enqueued: there a
+// launch may follow a kernel that wrote what its producer warp reads before
+// griddepcontrol.wait (the eta flag words of a chunk), so those launches are
+// plainly stream-ordered.
+thread_local bool g_plain_launches = false;
+
 template <typename Kern>
 void launch_pdl(Kern kernel, dim3 g, dim3 b, size_t smem, cudaStream_t st, const TmaStencilArgs& A) {
     cudaLaunchConfig_t cfg{};
@@ -667,7 +677,7 @@ void launch_pdl(Kern kernel, dim3 g, dim3 b, size_t smem, cudaStream_t st, const
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = pdl_enabled() && !g_plain_launches ? 1 : 0;
     SF_CUDA(cudaLaunchKernelEx(&cfg, kernel, A));
 }
 
@@ -1134,7 +1144,7 @@ void launch_stencil(const Plan& p, float* out, const float* cur, const float* pr
 }
 
 void launch_inject(const Plan& p, const PointSet& s, float* field, int64_t row, int first = 0,
-                   int count = -1) {
+                   int count = -1, int zf0 = 0, int zf1 = 0) {
     if (count < 0) count = s.ncells - first;
     if (count <= 0 || s.np == 0) return;
     InjectArgs A{};
@@ -1149,12 +1159,18 @@ void launch_inject(const Plan& p, const PointSet& s, float* field, int64_t row, 
     A.cell_off = s.cell_off + first;
     A.start = s.start + first;
     A.ncells = count;
+    A.plane = p.plane;
+    A.zf0 = zf0;
+    A.zf1 = zf1;
     inject_kernel<<<(count + 255) / 256, 256, 0, p.stream>>>(A);
 }
 
-void launch_sample(const Plan& p, const PointSet& s, const float* field, int64_t row) {
+void launch_sample(const Plan& p, const PointSet& s, const float* field, int64_t row, int zf0 = 0,
+                   int zf1 = 0) {
     if (s.np == 0) return;
     SampleArgs A{};
+    A.zf0 = zf0;
+    A.zf1 = zf1;
     A.field = field;
     A.ci = s.ci;
     A.w = s.w;
@@ -1766,8 +1782,9 @@ void ensure_fused(Plan& p) {
 // eta0 bits for one tile shape (see TmaStencilArgs::eta0): recomputed on the
 // plan stream when eta was rewritten or the tile shape changed; a new buffer
 // drops the cached graphs (they hold the pointer).
-void compute_eta_flags(Plan& p, sf_plan::EtaFlags& f, int tx, int ty) {
-    if (f.gen == p.eta_gen && f.tx == tx && f.ty == ty) return;
+// Sizes the flag words for the tile geometry; returns the number of 32-plane
+// groups. launch_eta_flags then fills groups [word0, word0 + nwords).
+int prepare_eta_flags(Plan& p, sf_plan::EtaFlags& f, int tx, int ty) {
     const int n0 = static_cast<int>(p.n[0]), n1 = static_cast<int>(p.n[1]),
               n2 = static_cast<int>(p.n[2]);
     const int ntx = (n2 + tx - 1) / tx, nty = (n1 + ty - 1) / ty, words = (n0 + 31) / 32;
@@ -1785,20 +1802,40 @@ void compute_eta_flags(Plan& p, sf_plan::EtaFlags& f, int tx, int ty) {
     f.ntx = ntx;
     f.nty = nty;
     f.words = words;
-    eta_zero_flags_kernel<<<dim3(static_cast<unsigned>(ntx * nty), static_cast<unsigned>(words)), 256,
-                            0, p.stream>>>(p.eta, p.pitch, p.plane, n0, n1, n2, tx, ty, ntx, words,
-                                           f.bits);
+    return words;
+}
+
+void launch_eta_flags(Plan& p, sf_plan::EtaFlags& f, int word0, int nwords) {
+    if (nwords <= 0) return;
+    eta_zero_flags_kernel<<<dim3(static_cast<unsigned>(f.ntx * f.nty), static_cast<unsigned>(nwords)),
+                            256, 0, p.stream>>>(p.eta, p.pitch, p.plane, static_cast<int>(p.n[0]),
+                                                static_cast<int>(p.n[1]), static_cast<int>(p.n[2]),
+                                                f.tx, f.ty, f.ntx, f.words, f.bits, word0);
     SF_CUDA(cudaGetLastError());
+}
+
+void compute_eta_flags(Plan& p, sf_plan::EtaFlags& f, int tx, int ty) {
+    if (f.gen == p.eta_gen && f.tx == tx && f.ty == ty) return;
+    const int words = prepare_eta_flags(p, f, tx, ty);
+    launch_eta_flags(p, f, 0, words);
     f.gen = p.eta_gen;
 }
 
+bool eta_flags_wanted(const Plan& p) {
+    return !(p.eta_skip_disabled || p.ndim != 3 || !p.eta || !(p.use_vec || p.use_vecq)) &&
+           (p.kind == Plan::ACOUSTIC || p.kind == Plan::FWI);
+}
+
+void eta_flag_tile(const Plan& p, int* tx, int* ty) {
+    *tx = p.use_vecq ? 64 : 32 * p.tile_nx;
+    *ty = p.use_vecq ? 2 * p.vec_warps : 4 * p.vec_warps * p.vec_rpl / p.tile_nx;
+}
+
 void ensure_eta_flags(Plan& p) {
-    if (p.eta_skip_disabled || p.ndim != 3 || !p.eta || !(p.use_vec || p.use_vecq)) return;
-    if (p.kind != Plan::ACOUSTIC && p.kind != Plan::FWI) return;
-    if (p.use_vecq)
-        compute_eta_flags(p, p.eta0, 64, 2 * p.vec_warps);
-    else
-        compute_eta_flags(p, p.eta0, 32 * p.tile_nx, 4 * p.vec_warps * p.vec_rpl / p.tile_nx);
+    if (!eta_flags_wanted(p)) return;
+    int tx, ty;
+    eta_flag_tile(p, &tx, &ty);
+    compute_eta_flags(p, p.eta0, tx, ty);
     if (p.kind == Plan::FWI) compute_eta_flags(p, p.eta0_grad, 64, 8);
 }
 
@@ -2191,6 +2228,167 @@ void download_acoustic(Plan& p, void* const* a) {
     SF_CUDA(cudaStreamSynchronize(p.stream));
 }
 
+// ---------------------------------------------------------------------------
+// sf_plan_invoke with the upload hidden behind the first time steps.
+//
+// The five fields (three time slots, m, eta) reach the GPU in chunks of whole
+// a0 planes on a copy stream. Step k needs u(t) only R planes beyond what it
+// updates, so while chunk c+1 is still on the PCIe link the first K steps
+// already run on the planes that have arrived, each trailing its predecessor
+// by R planes (a time-skewed sweep: step k may update plane z once step k-1
+// has finished planes < z + R + 1). Every point is still computed by the same
+// kernel from the same inputs, injection and sampling of a step are applied
+// to each plane range right after the step's stencil on it, in stream order,
+// so the result is bitwise the plain upload-then-run sequence
+// (tests/test_gpu_parity.py::test_invoke_overlapped_*). After the last chunk
+// the K steps are completed one after the other and steps K..nt run as the
+// usual captured graph. SF_NO_IO_OVERLAP=1 disables, SF_IO_CHUNK_PLANES /
+// SF_IO_STEPS override the chunk height (multiple of 32) and K.
+bool io_overlap_eligible(const Plan& p, void* const* a, int nargs) {
+    if (const char* e = std::getenv("SF_NO_IO_OVERLAP"))
+        if (e[0] == '1') return false;
+    if (p.kind != Plan::ACOUSTIC || p.ndim != 3 || p.slab || p.nccl_comm) return false;
+    if (!(p.use_tma && (p.use_vec || p.use_vecq))) return false;
+    if (nargs != 9 || !a[0] || !a[1] || !a[2]) return false;
+    const int r = p.ac.radius;
+    return p.nt >= 1 && p.n[0] > 32 && p.z1 - p.z0 >= 4 * r;
+}
+
+void tile_extent(const Plan& p, int64_t* wx, int64_t* wy) {
+    *wx = p.use_vecq ? 64 : 32 * p.tile_nx;
+    *wy = p.use_vecq ? 2 * p.vec_warps
+          : p.use_vec ? 4 * p.vec_warps * p.vec_rpl / p.tile_nx
+                      : p.tile_ty;
+}
+
+void h2d_planes(const Plan& p, float* dst, const float* src, int z0, int z1, cudaStream_t st) {
+    const int64_t n1 = p.n[1], n2 = p.n[2];
+    SF_CUDA(cudaMemcpy2DAsync(dst + static_cast<int64_t>(z0) * p.plane, sizeof(float) * p.pitch,
+                              src + static_cast<int64_t>(z0) * n1 * n2, sizeof(float) * n2,
+                              sizeof(float) * n2, static_cast<size_t>(z1 - z0) * n1,
+                              cudaMemcpyHostToDevice, st));
+}
+
+int64_t invoke_overlapped(Plan& p, void* const* a) {
+    const bool fwd = p.ac.forward;
+    const int r = p.ac.radius, n0 = static_cast<int>(p.n[0]);
+    const int zlo = p.z0, zhi = p.z1;
+    SF_CUDA(cudaSetDevice(p.device));
+    // point sets first (host-side CSR build, small copies on the compute stream)
+    upload_points(p, p.src, static_cast<const float*>(a[3]), static_cast<const int*>(a[4]),
+                  static_cast<const float*>(a[5]), fwd);
+    upload_points(p, p.rec, static_cast<const float*>(a[6]), static_cast<const int*>(a[7]),
+                  static_cast<const float*>(a[8]), !fwd);
+    const PointSet& inj = fwd ? p.src : p.rec;
+    const PointSet& smp = fwd ? p.rec : p.src;
+    auto c0_range = [&](const PointSet& s, int* lo, int* hi) {
+        *lo = INT32_MAX;
+        *hi = -1;
+        for (int64_t q = 0; q < s.np; ++q) {
+            const int c = s.host_ci[q * 3];
+            *lo = std::min(*lo, c);
+            *hi = std::max(*hi, c);
+        }
+    };
+    int inj_lo, inj_hi, smp_lo, smp_hi;  // lower corner planes of the point sets
+    c0_range(inj, &inj_lo, &inj_hi);
+    c0_range(smp, &smp_lo, &smp_hi);
+
+    // chunks of whole planes, a multiple of 32 (one eta flag word per 32 planes)
+    int zc = std::max(32, (n0 / 16 + 31) / 32 * 32);
+    if (const char* e = std::getenv("SF_IO_CHUNK_PLANES")) {
+        const int v = std::atoi(e);
+        if (v >= 32) zc = v / 32 * 32;
+    }
+    const int nchunks = (n0 + zc - 1) / zc;
+    int K = static_cast<int>(std::min<int64_t>(p.nt, 96));
+    if (const char* e = std::getenv("SF_IO_STEPS")) {
+        const int v = std::atoi(e);
+        if (v >= 1) K = static_cast<int>(std::min<int64_t>(p.nt, v));
+    }
+    K = std::max(1, std::min(K, (zhi - zlo) / r - 2));
+
+    if (!p.io) SF_CUDA(cudaStreamCreateWithFlags(&p.io, cudaStreamNonBlocking));
+    while (static_cast<int>(p.ev_up.size()) < nchunks) {
+        cudaEvent_t e;
+        SF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        p.ev_up.push_back(e);
+    }
+    // the copies start once whatever used the fields before has finished
+    SF_CUDA(cudaEventRecord(p.ev0, p.stream));
+    SF_CUDA(cudaStreamWaitEvent(p.io, p.ev0, 0));
+    const int64_t fe = field_numel(p);
+    for (int c = 0; c < nchunks; ++c) {
+        const int a0 = c * zc, a1 = std::min(n0, a0 + zc);
+        for (int s = 0; s < 3; ++s)
+            h2d_planes(p, p.slot[s], static_cast<const float*>(a[0]) + s * fe, a0, a1, p.io);
+        h2d_planes(p, p.m, static_cast<const float*>(a[1]), a0, a1, p.io);
+        h2d_planes(p, p.eta, static_cast<const float*>(a[2]), a0, a1, p.io);
+        SF_CUDA(cudaEventRecord(p.ev_up[c], p.io));
+    }
+    ++p.eta_gen;
+    const bool flags = eta_flags_wanted(p);
+    if (flags) {
+        int tx, ty;
+        eta_flag_tile(p, &tx, &ty);
+        prepare_eta_flags(p, p.eta0, tx, ty);
+        p.eta0.gen = p.eta_gen;  // filled chunk by chunk below, before any launch reads them
+    }
+
+    int64_t wx, wy;
+    tile_extent(p, &wx, &wy);
+    std::vector<int> front(static_cast<size_t>(K), zlo);
+    int64_t launches = 0;
+    // step k over planes [front[k], nf): stencil, then this step's injection
+    // into, and sampling on top of, exactly those planes
+    auto advance = [&](int k, int nf) {
+        const int f0 = front[k];
+        if (nf <= f0) return;
+        sf_plan::ZRange zr;
+        zr.z0 = f0;
+        zr.z1 = nf;
+        chunk_grid(p, wx, wy, p.resident, &zr.grid, &zr.zchunk, nf - f0);
+        const StepSlots st = step_slots(p, k, p.slot);
+        launch_stencil(p, st.out, st.cur, st.prev, nullptr, nullptr, &zr);
+        ++launches;
+        // planes outside the stencil's range belong to the first / last range
+        const int fa = f0 == zlo ? 0 : f0, fb = nf == zhi ? n0 + 1 : nf;
+        if (inj.np > 0 && inj.ncells > 0 && inj_hi + 1 >= fa && inj_lo < fb) {
+            launch_inject(p, inj, st.out, st.row, 0, -1, fa, fb);
+            ++launches;
+        }
+        if (smp.np > 0 && smp_hi + 1 >= fa && smp_lo + 1 < fb) {
+            launch_sample(p, smp, st.out, st.row, std::max(fa, 1), fb);
+            ++launches;
+        }
+        front[k] = nf;
+    };
+    g_plain_launches = true;
+    try {
+        for (int c = 0; c < nchunks; ++c) {
+            const int up = std::min(n0, (c + 1) * zc);  // planes [0, up) have arrived
+            SF_CUDA(cudaStreamWaitEvent(p.stream, p.ev_up[c], 0));
+            if (flags) launch_eta_flags(p, p.eta0, c * zc / 32, (up - c * zc + 31) / 32);
+            for (int k = 0; k < K; ++k) {
+                // u(t) of step k is valid below `avail`: the upload for k = 0,
+                // else what step k-1 has finished (plus the static planes
+                // beyond the interior once everything has arrived)
+                const int avail = k == 0 ? up : front[k - 1] < zhi ? front[k - 1] : up == n0 ? n0 : zhi;
+                const int nf = std::min(zhi, avail - r);
+                if (nf <= front[k]) break;  // later steps trail this one
+                advance(k, nf);
+            }
+        }
+        for (int k = 0; k < K; ++k) advance(k, zhi);  // complete the skewed steps in order
+    } catch (...) {
+        g_plain_launches = false;
+        throw;
+    }
+    g_plain_launches = false;
+    run_steps(p, K, p.nt);
+    return launches;
+}
+
 void upload_any(Plan& p, void* const* a, int nargs) {
     if (nargs != static_cast<int>(p.arg_names.size()))
         throw Status(SF_ERR_SIGNATURE, "expected " + std::to_string(p.arg_names.size()) +
@@ -2273,6 +2471,8 @@ sf_plan::~sf_plan() {
     sfb::dfree(hist);
     sfb::dfree(grad);
     for (float* s : v) sfb::dfree(s);
+    for (cudaEvent_t e : ev_up) cudaEventDestroy(e);
+    if (io) cudaStreamDestroy(io);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (ev_copy) cudaEventDestroy(ev_copy);
@@ -2969,11 +3169,15 @@ int sf_plan_invoke(sf_plan* p, void* const* args, int nargs) {
         for (int i = 0; i < nargs; ++i)
             if (!args[i]) throw Status(SF_ERR_SIGNATURE, "null buffer for " + p->arg_names.at(i));
         sfb::NvtxRange whole("sf_plan_invoke");
-        {
-            sfb::NvtxRange r("upload (H2D + repack)");
-            sfb::upload_any(*p, args, nargs);
-        }
-        {
+        if (sfb::io_overlap_eligible(*p, args, nargs)) {
+            sfb::NvtxRange r("upload overlapped by the first time steps + time loop");
+            sfb::invoke_overlapped(*p, args);
+            sfb::check_kernel_errors(*p);
+        } else {
+            {
+                sfb::NvtxRange r("upload (H2D + repack)");
+                sfb::upload_any(*p, args, nargs);
+            }
             sfb::NvtxRange r("time loop");
             sfb::run_steps(*p, 0, p->nt);
             sfb::check_kernel_errors(*p);

@@ -796,3 +796,60 @@ def test_zero_eta_boxes_special_values(sf, port, order, forward):
     assert np.array_equal(np.isfinite(out[0]), fin)
     assert np.array_equal(bits(out[0])[fin], bits(u)[fin])
     assert (~fin).any() and fin.sum() > 0.2 * fin.size
+
+
+@pytest.mark.parametrize("order", [4, 8, 12, 16])
+@pytest.mark.parametrize("forward", [True, False])
+@pytest.mark.parametrize("knobs", [{}, {"SF_IO_STEPS": "1"}, {"SF_IO_STEPS": "3"},
+                                   {"SF_IO_STEPS": "50"}, {"SF_IO_CHUNK_PLANES": "64"},
+                                   {"SF_NO_IO_OVERLAP": "1"}],
+                         ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()) or "auto")
+def test_invoke_overlapped_upload_bitwise(sf, port, monkeypatch, order, forward, knobs):
+    """sf_acoustic_apply with the upload hidden behind the first time steps
+    (plane chunks on a copy stream, the first K steps time-skewed behind the
+    upload front, plan.cu invoke_overlapped): bitwise the oracle for every
+    chunking and K, with a random initial state in all three slots and point
+    sets spread over every plane -- the boundary strips the stencil never
+    writes, chunk seams, colliding cells -- so injection and sampling per plane
+    range are exercised in both directions."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    r = order // 2
+    shape = (131, 30, 70)  # five 32-plane chunks (the last one partial)
+    nt = 19
+    rng = np.random.default_rng(1000 + order + forward)
+    v = 1500.0 + 3000.0 * rng.random(shape)
+    m, eta = port.medium_from_velocity(v, 5, 10.0, 1500.0)
+    dt = min(0.4 * 10.0 / 4500.0, port.stable_dt(3, order, 10.0, 4500.0, 4500.0))
+
+    def pts(n):
+        c = np.stack([rng.uniform(0.0, (e - 1.001) * 10.0, n) for e in shape], 1)
+        # planes next to both faces, on chunk seams and in the middle
+        z = np.concatenate([[0.2, 1.5, r - 0.5, r + 0.5, 30.7, 31.5, 32.2, 63.9, 95.5, 127.1,
+                             shape[0] - r - 1.5, shape[0] - r - 0.5, shape[0] - 1.9],
+                            rng.uniform(0.0, shape[0] - 1.001, max(0, n - 13))])[:n]
+        c[:, 0] = z * 10.0
+        return c
+    src_c, rec_c = pts(21), pts(40)
+    src_c[1] = src_c[0] + 0.1 * 10.0 * rng.random(3) * [0.0, 1.0, 1.0]  # shared cells
+    src_ci, src_w = port.interp(src_c, 10.0, shape)
+    rec_ci, rec_w = port.interp(rec_c, 10.0, shape)
+    u0 = (1e-3 * rng.standard_normal((3,) + shape)).astype(np.float32)
+    if forward:
+        src = rng.standard_normal((nt, 21)).astype(np.float32)
+        rec = np.zeros((nt, 40), np.float32)
+    else:
+        src = np.zeros((nt, 21), np.float32)
+        rec = rng.standard_normal((nt, 40)).astype(np.float32)
+    out = run_plan_raw(sf, shape, order, forward, dt, 10.0, nt, m, eta, src.copy(), src_ci, src_w,
+                       rec.copy(), rec_ci, rec_w, u=u0.copy())
+    coefs = port.coefs(3, order, forward, dt, 10.0)
+    u = u0.copy()
+    if forward:
+        port.acoustic_run(coefs, u, m, eta, src, src_ci, src_w, rec, rec_ci, rec_w, nt)
+        assert_parity(out[6], rec)
+    else:
+        port.acoustic_run(coefs, u, m, eta, rec, rec_ci, rec_w, src, src_ci, src_w, nt)
+        assert_parity(out[3], src)
+    assert_parity(out[0], u)
+    assert np.abs(u).max() > 0
