@@ -2242,16 +2242,49 @@ void download_acoustic(Plan& p, void* const* a) {
 // so the result is bitwise the plain upload-then-run sequence
 // (tests/test_gpu_parity.py::test_invoke_overlapped_*). After the last chunk
 // the K steps are completed one after the other and steps K..nt run as the
-// usual captured graph. SF_NO_IO_OVERLAP=1 disables, SF_IO_CHUNK_PLANES /
-// SF_IO_STEPS override the chunk height (multiple of 32) and K.
+// usual captured graph; the last K2 steps are skewed again so that low planes
+// become final first and travel back while the rest finishes. Used where a
+// chunk of a step is long against a kernel launch (io_overlap_eligible).
+// SF_NO_IO_OVERLAP=1 disables, SF_IO_OVERLAP=1 forces it at any size (tests),
+// SF_IO_CHUNK_PLANES / SF_IO_STEPS / SF_IO_TAIL_STEPS override the chunk
+// height (multiple of 32), K and K2.
+// Rough times the decisions below rest on: a memory-bound time step (20 B per
+// interior point at ~5.5 TB/s) and the PCIe link at ~55 GB/s.
+double step_seconds_estimate(const Plan& p) {
+    const int r = p.ac.radius;
+    const double pts = static_cast<double>(p.n[0] - 2 * r) * static_cast<double>(p.n[1] - 2 * r) *
+                       static_cast<double>(p.n[2] - 2 * r);
+    return pts * 20.0 / 5.5e12;
+}
+
+// Chunk height: whole planes, a multiple of 32 (one eta flag word per 32
+// planes), about n0 / 16, and tall enough that one step on one chunk runs for
+// ~100 us (the skewed steps are plain launches, not graph nodes).
+int io_chunk_planes(const Plan& p) {
+    const int n0 = static_cast<int>(p.n[0]);
+    if (const char* e = std::getenv("SF_IO_CHUNK_PLANES")) {
+        const int v = std::atoi(e);
+        if (v >= 32) return v / 32 * 32;
+    }
+    const double per_plane = step_seconds_estimate(p) / n0;
+    const int by_time = static_cast<int>(100e-6 / std::max(per_plane, 1e-12)) + 1;
+    return (std::max({32, n0 / 16, by_time}) + 31) / 32 * 32;
+}
+
 bool io_overlap_eligible(const Plan& p, void* const* a, int nargs) {
+    bool forced = false;
     if (const char* e = std::getenv("SF_NO_IO_OVERLAP"))
         if (e[0] == '1') return false;
+    if (const char* e = std::getenv("SF_IO_OVERLAP")) forced = e[0] == '1';  // tests: any size
     if (p.kind != Plan::ACOUSTIC || p.ndim != 3 || p.slab || p.nccl_comm) return false;
     if (!(p.use_tma && (p.use_vec || p.use_vecq))) return false;
     if (nargs != 9 || !a[0] || !a[1] || !a[2]) return false;
     const int r = p.ac.radius;
-    return p.nt >= 1 && p.n[0] > 32 && p.z1 - p.z0 >= 4 * r;
+    if (!(p.nt >= 1 && p.n[0] > 32 && p.z1 - p.z0 >= 4 * r)) return false;
+    // worth it only where a chunk of a step is long against a launch: at least
+    // four chunks (measured: 281^3 with 32-plane chunks loses 40 %, 1024^3
+    // with 64-plane chunks gains 10 %)
+    return forced || 4 * io_chunk_planes(p) <= p.n[0];
 }
 
 void tile_extent(const Plan& p, int64_t* wx, int64_t* wy) {
@@ -2263,6 +2296,13 @@ void tile_extent(const Plan& p, int64_t* wx, int64_t* wy) {
 
 void h2d_planes(const Plan& p, float* dst, const float* src, int z0, int z1, cudaStream_t st) {
     const int64_t n1 = p.n[1], n2 = p.n[2];
+    if (p.pitch == n2) {  // dense rows: one contiguous transfer
+        SF_CUDA(cudaMemcpyAsync(dst + static_cast<int64_t>(z0) * p.plane,
+                                src + static_cast<int64_t>(z0) * n1 * n2,
+                                sizeof(float) * static_cast<size_t>(z1 - z0) * n1 * n2,
+                                cudaMemcpyHostToDevice, st));
+        return;
+    }
     SF_CUDA(cudaMemcpy2DAsync(dst + static_cast<int64_t>(z0) * p.plane, sizeof(float) * p.pitch,
                               src + static_cast<int64_t>(z0) * n1 * n2, sizeof(float) * n2,
                               sizeof(float) * n2, static_cast<size_t>(z1 - z0) * n1,
@@ -2294,14 +2334,14 @@ int64_t invoke_overlapped(Plan& p, void* const* a) {
     c0_range(inj, &inj_lo, &inj_hi);
     c0_range(smp, &smp_lo, &smp_hi);
 
-    // chunks of whole planes, a multiple of 32 (one eta flag word per 32 planes)
-    int zc = std::max(32, (n0 / 16 + 31) / 32 * 32);
-    if (const char* e = std::getenv("SF_IO_CHUNK_PLANES")) {
-        const int v = std::atoi(e);
-        if (v >= 32) zc = v / 32 * 32;
-    }
+    const int zc = io_chunk_planes(p);
     const int nchunks = (n0 + zc - 1) / zc;
-    int K = static_cast<int>(std::min<int64_t>(p.nt, 96));
+    // steps worth of compute that fit under the upload / the copy back
+    const double t_step = step_seconds_estimate(p);
+    const double field_bytes = 4.0 * static_cast<double>(p.n[0]) * p.n[1] * p.n[2];
+    const int k_up = static_cast<int>(5.0 * field_bytes / 55e9 / t_step) + 1;
+    const int k_down = static_cast<int>(1.2 * 3.0 * field_bytes / 55e9 / t_step) + 1;
+    int K = static_cast<int>(std::min<int64_t>(p.nt, std::min(k_up, 128)));
     if (const char* e = std::getenv("SF_IO_STEPS")) {
         const int v = std::atoi(e);
         if (v >= 1) K = static_cast<int>(std::min<int64_t>(p.nt, v));
@@ -2335,14 +2375,22 @@ int64_t invoke_overlapped(Plan& p, void* const* a) {
         p.eta0.gen = p.eta_gen;  // filled chunk by chunk below, before any launch reads them
     }
 
+    // the last K2 steps run skewed the other way round (below): low planes
+    // become final first and go back to the host while the rest finishes
+    int K2 = static_cast<int>(std::min<int64_t>(p.nt - K, std::min(k_down, 96)));
+    if (const char* e = std::getenv("SF_IO_TAIL_STEPS")) {
+        const int v = std::atoi(e);
+        if (v >= 0) K2 = static_cast<int>(std::min<int64_t>(p.nt - K, v));
+    }
+    K2 = std::max(0, K2);
+
     int64_t wx, wy;
     tile_extent(p, &wx, &wy);
-    std::vector<int> front(static_cast<size_t>(K), zlo);
     int64_t launches = 0;
-    // step k over planes [front[k], nf): stencil, then this step's injection
+    // step k over planes [*front, nf): stencil, then this step's injection
     // into, and sampling on top of, exactly those planes
-    auto advance = [&](int k, int nf) {
-        const int f0 = front[k];
+    auto advance = [&](int64_t k, int* front, int nf) {
+        const int f0 = *front;
         if (nf <= f0) return;
         sf_plan::ZRange zr;
         zr.z0 = f0;
@@ -2361,10 +2409,15 @@ int64_t invoke_overlapped(Plan& p, void* const* a) {
             launch_sample(p, smp, st.out, st.row, std::max(fa, 1), fb);
             ++launches;
         }
-        front[k] = nf;
+        *front = nf;
     };
-    g_plain_launches = true;
-    try {
+    struct PlainLaunches {  // see g_plain_launches
+        PlainLaunches() { g_plain_launches = true; }
+        ~PlainLaunches() { g_plain_launches = false; }
+    };
+    {
+        PlainLaunches plain;
+        std::vector<int> front(static_cast<size_t>(K), zlo);
         for (int c = 0; c < nchunks; ++c) {
             const int up = std::min(n0, (c + 1) * zc);  // planes [0, up) have arrived
             SF_CUDA(cudaStreamWaitEvent(p.stream, p.ev_up[c], 0));
@@ -2376,17 +2429,48 @@ int64_t invoke_overlapped(Plan& p, void* const* a) {
                 const int avail = k == 0 ? up : front[k - 1] < zhi ? front[k - 1] : up == n0 ? n0 : zhi;
                 const int nf = std::min(zhi, avail - r);
                 if (nf <= front[k]) break;  // later steps trail this one
-                advance(k, nf);
+                advance(k, &front[k], nf);
             }
         }
-        for (int k = 0; k < K; ++k) advance(k, zhi);  // complete the skewed steps in order
-    } catch (...) {
-        g_plain_launches = false;
-        throw;
+        for (int k = 0; k < K; ++k) advance(k, &front[k], zhi);  // complete the skewed steps in order
     }
-    g_plain_launches = false;
-    run_steps(p, K, p.nt);
-    return launches;
+    run_steps(p, K, p.nt - K2);
+    if (K2 == 0) return launches;
+
+    // Tail: chunk c of the three slots is final once the last step has
+    // finished its planes, which needs step nt-1-i to be r * i planes further.
+    // Each pass advances all K2 steps just that far, then the chunk's copy
+    // back starts on the copy stream while the next pass runs.
+    {
+        PlainLaunches plain;
+        std::vector<int> front(static_cast<size_t>(K2), zlo);
+        float* host_u = static_cast<float*>(a[0]);
+        for (int c = 0; c < nchunks; ++c) {
+            const int c0 = c * zc, c1 = std::min(n0, c0 + zc);
+            for (int j = 0; j < K2; ++j) {
+                const int target = c1 >= zhi ? zhi : std::min(zhi, c1 + r * (K2 - 1 - j));
+                advance(p.nt - K2 + j, &front[j], target);
+            }
+            SF_CUDA(cudaEventRecord(p.ev_up[c], p.stream));
+            SF_CUDA(cudaStreamWaitEvent(p.io, p.ev_up[c], 0));
+            for (int sl = 0; sl < 3; ++sl)
+                if (p.pitch == p.n[2])
+                    SF_CUDA(cudaMemcpyAsync(host_u + sl * fe + static_cast<int64_t>(c0) * p.plane,
+                                            p.slot[sl] + static_cast<int64_t>(c0) * p.plane,
+                                            sizeof(float) * static_cast<size_t>(c1 - c0) * p.plane,
+                                            cudaMemcpyDeviceToHost, p.io));
+                else
+                SF_CUDA(cudaMemcpy2DAsync(host_u + sl * fe + static_cast<int64_t>(c0) * p.n[1] * p.n[2],
+                                          sizeof(float) * p.n[2],
+                                          p.slot[sl] + static_cast<int64_t>(c0) * p.plane,
+                                          sizeof(float) * p.pitch, sizeof(float) * p.n[2],
+                                          static_cast<size_t>(c1 - c0) * p.n[1],
+                                          cudaMemcpyDeviceToHost, p.io));
+        }
+        SF_CUDA(cudaEventRecord(p.ev_up[0], p.io));
+        SF_CUDA(cudaStreamWaitEvent(p.stream, p.ev_up[0], 0));  // the call ends when the copies have
+    }
+    return -launches;  // negative: the field is already back in host memory
 }
 
 void upload_any(Plan& p, void* const* a, int nargs) {
@@ -3169,9 +3253,10 @@ int sf_plan_invoke(sf_plan* p, void* const* args, int nargs) {
         for (int i = 0; i < nargs; ++i)
             if (!args[i]) throw Status(SF_ERR_SIGNATURE, "null buffer for " + p->arg_names.at(i));
         sfb::NvtxRange whole("sf_plan_invoke");
+        bool field_back = false;
         if (sfb::io_overlap_eligible(*p, args, nargs)) {
-            sfb::NvtxRange r("upload overlapped by the first time steps + time loop");
-            sfb::invoke_overlapped(*p, args);
+            sfb::NvtxRange r("time loop with the upload / download overlapped by its first / last steps");
+            field_back = sfb::invoke_overlapped(*p, args) < 0;
             sfb::check_kernel_errors(*p);
         } else {
             {
@@ -3190,6 +3275,7 @@ int sf_plan_invoke(sf_plan* p, void* const* args, int nargs) {
         if (p->kind == sf_plan::ACOUSTIC)
             for (int i = 1; i < nargs; ++i)
                 if (i != (p->ac.forward ? 6 : 3)) out[i] = nullptr;
+        if (field_back) out[0] = nullptr;
         sfb::download_any(*p, out.data(), nargs);
     });
 }

@@ -802,16 +802,24 @@ def test_zero_eta_boxes_special_values(sf, port, order, forward):
 @pytest.mark.parametrize("forward", [True, False])
 @pytest.mark.parametrize("knobs", [{}, {"SF_IO_STEPS": "1"}, {"SF_IO_STEPS": "3"},
                                    {"SF_IO_STEPS": "50"}, {"SF_IO_CHUNK_PLANES": "64"},
+                                   {"SF_IO_STEPS": "4", "SF_IO_TAIL_STEPS": "0"},
+                                   {"SF_IO_STEPS": "4", "SF_IO_TAIL_STEPS": "1"},
+                                   {"SF_IO_STEPS": "4", "SF_IO_TAIL_STEPS": "2"},
+                                   {"SF_IO_STEPS": "6", "SF_IO_TAIL_STEPS": "7",
+                                    "SF_IO_CHUNK_PLANES": "64"},
                                    {"SF_NO_IO_OVERLAP": "1"}],
                          ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()) or "auto")
 def test_invoke_overlapped_upload_bitwise(sf, port, monkeypatch, order, forward, knobs):
     """sf_acoustic_apply with the upload hidden behind the first time steps
     (plane chunks on a copy stream, the first K steps time-skewed behind the
-    upload front, plan.cu invoke_overlapped): bitwise the oracle for every
-    chunking and K, with a random initial state in all three slots and point
+    upload front, plan.cu invoke_overlapped) and the copy back hidden behind
+    the last K2 steps (skewed so low planes become final first; with K = 1 or
+    3 of the 19 steps the tail takes all the others): bitwise the oracle for
+    every chunking, K and K2, with a random initial state in all three slots and point
     sets spread over every plane -- the boundary strips the stencil never
     writes, chunk seams, colliding cells -- so injection and sampling per plane
     range are exercised in both directions."""
+    monkeypatch.setenv("SF_IO_OVERLAP", "1")  # small grids take the plain path by default
     for k, v in knobs.items():
         monkeypatch.setenv(k, v)
     r = order // 2
