@@ -2281,10 +2281,21 @@ bool io_overlap_eligible(const Plan& p, void* const* a, int nargs) {
     if (nargs != 9 || !a[0] || !a[1] || !a[2]) return false;
     const int r = p.ac.radius;
     if (!(p.nt >= 1 && p.n[0] > 32 && p.z1 - p.z0 >= 4 * r)) return false;
+    if (forced) return true;
+    // asynchronous copies need page-locked host buffers (pageable ones are
+    // staged synchronously: correct, but nothing would overlap)
+    for (int i = 0; i < 3; ++i) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, a[i]) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        if (at.type != cudaMemoryTypeHost) return false;
+    }
     // worth it only where a chunk of a step is long against a launch: at least
     // four chunks (measured: 281^3 with 32-plane chunks loses 40 %, 1024^3
     // with 64-plane chunks gains 10 %)
-    return forced || 4 * io_chunk_planes(p) <= p.n[0];
+    return 4 * io_chunk_planes(p) <= p.n[0];
 }
 
 void tile_extent(const Plan& p, int64_t* wx, int64_t* wy) {

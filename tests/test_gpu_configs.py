@@ -257,7 +257,14 @@ def _full_loop_vs_reference(sf, ref, name, nt=None):
     if nt is not None:
         w.nt = nt
     s = sf.acoustic_build(model_of(sf, w), True, smooth=smooth_of(sf, w))
-    s.op.apply()
+    # through sf_plan_invoke's overlapped upload / copy back (the default for
+    # page-locked buffers at these sizes; forced here for the pageable ones)
+    import os
+    os.environ["SF_IO_OVERLAP"] = "1"
+    try:
+        s.op.apply()
+    finally:
+        del os.environ["SF_IO_OVERLAP"]
     ref.set_threads(ref.max_threads())
     op = ref_acoustic(ref, AcousticCase(shape=w.shape, nt=w.nt, boundary_width=w.bw,
                                         spacing=w.h, dt=w.dt, space_order=w.order, f0=w.f0,
