@@ -166,6 +166,11 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            # a timed region shorter than nvidia-smi's start-up (C1: ~13 ms)
+            # would leave no sample: take the first one it prints
+            t_end = time.time() + 3.0
+            while not self.lines and time.time() < t_end and self.proc.poll() is None:
+                time.sleep(0.05)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -664,7 +669,11 @@ def run_b200_fwi(args, local):
     src = np.array([sf.ricker_wavelet(10.0, t * dt, t0) for t in range(nt)], np.float32)[:, None]
     rng = np.random.default_rng(5)
     residual = rng.standard_normal((nt, len(rec_c)), dtype=np.float32)
-    plan = sf.FwiPlan(shape, order, nt, dt, H, 1, len(rec_c), device=local)
+    plan = sf.FwiPlan(shape, order, nt, dt, H, 1, len(rec_c), device=local, pinned=True)
+    # inputs resident in page-locked host memory, outputs into the plan's
+    # page-locked buffers: the copies inside the timed call run at the PCIe rate
+    m, eta, residual, src = (sf.api.pinned_array(x.shape, np.float32, like=x)
+                             for x in (m, eta, residual, src))
     # warm-up call (graph capture, sparse index build), then the timed one
     plan.gradient(m, eta, src, src_ci, src_w, rec_ci, rec_w, residual)
     t_e = time.perf_counter()

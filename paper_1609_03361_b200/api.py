@@ -86,6 +86,22 @@ def check(rc: int):
 # ---------------------------------------------------------------------------
 # grid data (grid.hpp:32-139)
 
+def pinned_array(shape, dtype=np.float32, like=None):
+    """Page-locked host array (numpy view of a pinned torch tensor; torch is
+    plumbing only): async H2D / D2H copies run at the PCIe rate from these."""
+    import torch
+    tdt = {np.float32: torch.float32, np.int32: torch.int32}[np.dtype(dtype).type]
+    t = torch.zeros(tuple(shape), dtype=tdt, pin_memory=True)
+    a = t.numpy()
+    _PINNED_KEEPALIVE[id(a)] = t
+    if like is not None:
+        a[...] = like
+    return a
+
+
+_PINNED_KEEPALIVE = {}
+
+
 class GridFunction:
     """Named buffer in the reference's dense layout (slot slowest)."""
 
@@ -714,7 +730,11 @@ class FwiPlan:
     """Forward with the full wavefield history in HBM, then the adjoint sweep
     fused with grad += u(t) * v_tt(t)."""
 
-    def __init__(self, shape, space_order, nt, dt, spacing, n_src, n_rec, device=0):
+    def __init__(self, shape, space_order, nt, dt, spacing, n_src, n_rec, device=0, pinned=False):
+        """pinned: keep page-locked host buffers for the outputs (reused by
+        every gradient() call, so copy what must outlive the next call)."""
+        self._pinned = pinned
+        self._out = {}
         desc = _lib.AcousticDesc()
         desc.ndim = 3
         for i, e in enumerate(shape):
@@ -759,13 +779,20 @@ class FwiPlan:
             if a.size != int(np.prod(shp)):
                 raise InvalidShapeError(f"{name} must have {int(np.prod(shp))} elements "
                                         f"{shp}, got {a.size}")
-        rec_out = np.zeros((self.nt, self.n_rec), np.float32)
-        grad = np.zeros(self.shape, np.float32)
-        v = np.zeros((3,) + self.shape, np.float32) if want_v else None
-        srcs = np.zeros((self.nt, self.n_src), np.float32) if want_src else None
+        rec_out = self._host("rec_out", (self.nt, self.n_rec))
+        grad = self._host("grad", self.shape)
+        v = self._host("v", (3,) + self.shape) if want_v else None
+        srcs = self._host("srcs", (self.nt, self.n_src)) if want_src else None
         check(lib.sf_fwi_gradient(self._plan, *[a.ctypes.data for a in ins], rec_out.ctypes.data,
                                   grad.ctypes.data, _lib.ptr(v), _lib.ptr(srcs)))
         return rec_out, grad, v, srcs
+
+    def _host(self, name, shape):
+        if not self._pinned:
+            return np.zeros(shape, np.float32)
+        if name not in self._out:
+            self._out[name] = pinned_array(shape, np.float32)
+        return self._out[name]
 
     def time(self):
         f = C.c_float()
