@@ -2314,10 +2314,32 @@ void h2d_planes(const Plan& p, float* dst, const float* src, int z0, int z1, cud
                                 cudaMemcpyHostToDevice, st));
         return;
     }
-    SF_CUDA(cudaMemcpy2DAsync(dst + static_cast<int64_t>(z0) * p.plane, sizeof(float) * p.pitch,
-                              src + static_cast<int64_t>(z0) * n1 * n2, sizeof(float) * n2,
-                              sizeof(float) * n2, static_cast<size_t>(z1 - z0) * n1,
-                              cudaMemcpyHostToDevice, st));
+    // padded rows: one contiguous transfer into the staging field, then a
+    // device repack on the same stream (row-by-row 2D copies over PCIe are
+    // several times slower for ~1 KB rows)
+    const int64_t rows = static_cast<int64_t>(z1 - z0) * n1;
+    SF_CUDA(cudaMemcpyAsync(p.staging, src + static_cast<int64_t>(z0) * n1 * n2,
+                            sizeof(float) * rows * n2, cudaMemcpyHostToDevice, st));
+    repack_rows_kernel<<<repack_grid(rows), 256, 0, st>>>(dst + static_cast<int64_t>(z0) * p.plane,
+                                                         p.pitch, p.staging, n2, rows,
+                                                         static_cast<int>(n2));
+}
+
+void d2h_planes(const Plan& p, float* dst, const float* src, int z0, int z1, cudaStream_t st) {
+    const int64_t n1 = p.n[1], n2 = p.n[2];
+    if (p.pitch == n2) {
+        SF_CUDA(cudaMemcpyAsync(dst + static_cast<int64_t>(z0) * p.plane,
+                                src + static_cast<int64_t>(z0) * p.plane,
+                                sizeof(float) * static_cast<size_t>(z1 - z0) * p.plane,
+                                cudaMemcpyDeviceToHost, st));
+        return;
+    }
+    const int64_t rows = static_cast<int64_t>(z1 - z0) * n1;
+    repack_rows_kernel<<<repack_grid(rows), 256, 0, st>>>(p.staging, n2,
+                                                         src + static_cast<int64_t>(z0) * p.plane,
+                                                         p.pitch, rows, static_cast<int>(n2));
+    SF_CUDA(cudaMemcpyAsync(dst + static_cast<int64_t>(z0) * n1 * n2, p.staging,
+                            sizeof(float) * rows * n2, cudaMemcpyDeviceToHost, st));
 }
 
 int64_t invoke_overlapped(Plan& p, void* const* a) {
@@ -2464,19 +2486,7 @@ int64_t invoke_overlapped(Plan& p, void* const* a) {
             }
             SF_CUDA(cudaEventRecord(p.ev_up[c], p.stream));
             SF_CUDA(cudaStreamWaitEvent(p.io, p.ev_up[c], 0));
-            for (int sl = 0; sl < 3; ++sl)
-                if (p.pitch == p.n[2])
-                    SF_CUDA(cudaMemcpyAsync(host_u + sl * fe + static_cast<int64_t>(c0) * p.plane,
-                                            p.slot[sl] + static_cast<int64_t>(c0) * p.plane,
-                                            sizeof(float) * static_cast<size_t>(c1 - c0) * p.plane,
-                                            cudaMemcpyDeviceToHost, p.io));
-                else
-                SF_CUDA(cudaMemcpy2DAsync(host_u + sl * fe + static_cast<int64_t>(c0) * p.n[1] * p.n[2],
-                                          sizeof(float) * p.n[2],
-                                          p.slot[sl] + static_cast<int64_t>(c0) * p.plane,
-                                          sizeof(float) * p.pitch, sizeof(float) * p.n[2],
-                                          static_cast<size_t>(c1 - c0) * p.n[1],
-                                          cudaMemcpyDeviceToHost, p.io));
+            for (int sl = 0; sl < 3; ++sl) d2h_planes(p, host_u + sl * fe, p.slot[sl], c0, c1, p.io);
         }
         SF_CUDA(cudaEventRecord(p.ev_up[0], p.io));
         SF_CUDA(cudaStreamWaitEvent(p.stream, p.ev_up[0], 0));  // the call ends when the copies have
@@ -3267,7 +3277,14 @@ int sf_plan_invoke(sf_plan* p, void* const* args, int nargs) {
         bool field_back = false;
         if (sfb::io_overlap_eligible(*p, args, nargs)) {
             sfb::NvtxRange r("time loop with the upload / download overlapped by its first / last steps");
-            field_back = sfb::invoke_overlapped(*p, args) < 0;
+            try {
+                field_back = sfb::invoke_overlapped(*p, args) < 0;
+            } catch (...) {
+                // asynchronous copies may still reference the caller's buffers
+                if (p->io) cudaStreamSynchronize(p->io);
+                cudaStreamSynchronize(p->stream);
+                throw;
+            }
             sfb::check_kernel_errors(*p);
         } else {
             {
