@@ -2259,7 +2259,7 @@ double step_seconds_estimate(const Plan& p) {
 
 // Chunk height: whole planes, a multiple of 32 (one eta flag word per 32
 // planes), about n0 / 16, and tall enough that one step on one chunk runs for
-// ~100 us (the skewed steps are plain launches, not graph nodes).
+// ~50 us (the skewed steps are plain launches, not graph nodes).
 int io_chunk_planes(const Plan& p) {
     const int n0 = static_cast<int>(p.n[0]);
     if (const char* e = std::getenv("SF_IO_CHUNK_PLANES")) {
@@ -2267,7 +2267,7 @@ int io_chunk_planes(const Plan& p) {
         if (v >= 32) return v / 32 * 32;
     }
     const double per_plane = step_seconds_estimate(p) / n0;
-    const int by_time = static_cast<int>(100e-6 / std::max(per_plane, 1e-12)) + 1;
+    const int by_time = static_cast<int>(50e-6 / std::max(per_plane, 1e-12)) + 1;
     return (std::max({32, n0 / 16, by_time}) + 31) / 32 * 32;
 }
 
