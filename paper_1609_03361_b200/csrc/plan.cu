@@ -121,6 +121,10 @@ struct PointSet {
 
 } // namespace sfb
 
+// rows-per-lane selector of the 16-warp radius-4 ring kernel with the a0
+// register queue (one row per lane)
+constexpr int kRplAq = 17;
+
 struct sf_plan {
     enum Kind { ACOUSTIC, DIFFUSION, FWI } kind;
     int device = 0;
@@ -163,7 +167,8 @@ struct sf_plan {
     int vec_warps = 8;
     int vec_rpl = 1;  // vector kernel: rows of four points per lane (1 or 2)
     bool vec_aq = true;  // 16-warp radius-4 ring kernel with the a0 register queue (SF_VEC_AQ=0: ring loads)
-    int vec_kernel_rpl() const { return vec_aq && vec_warps == 16 && vec_rpl == 1 ? 17 : vec_rpl; }
+    // kernel selector: kRplAq picks the a0-queue instance (geometry as rpl = 1)
+    int vec_kernel_rpl() const { return vec_aq && vec_warps == 16 && vec_rpl == 1 ? kRplAq : vec_rpl; }
     int tma_stages = 4;
     int stages_override = 0;  // autotune: > 0 forces the pipeline depth
     size_t tma_smem = 0;
@@ -517,10 +522,6 @@ size_t tma_smem_bytes(int r, int nx, int stages) {
 // (16 lanes per row), 1 -> 32-wide (8 lanes per row); rpl = rows per lane.
 // Compiled shapes (warps, nx, rpl): (4,2,1) (8,2,1) (4,1,1) (8,1,1) (2,1,2) (4,2,2), and
 // (16,2,1) at radius 4.
-// rows-per-lane code of the 16-warp radius-4 kernel with the a0 register
-// queue (one row per lane; geometry as rpl = 1)
-constexpr int kRplAq = 17;
-
 template <bool FWD, int RR>
 const void* vec_ptr_r(int warps, int nx, int rpl) {
     if (rpl == 2) {
@@ -2342,7 +2343,9 @@ void d2h_planes(const Plan& p, float* dst, const float* src, int z0, int z1, cud
                             sizeof(float) * rows * n2, cudaMemcpyDeviceToHost, st));
 }
 
-int64_t invoke_overlapped(Plan& p, void* const* a) {
+// Returns true when the three slots are already back in host memory (the tail
+// ran; false when nt left no steps for it).
+bool invoke_overlapped(Plan& p, void* const* a) {
     const bool fwd = p.ac.forward;
     const int r = p.ac.radius, n0 = static_cast<int>(p.n[0]);
     const int zlo = p.z0, zhi = p.z1;
@@ -2419,7 +2422,6 @@ int64_t invoke_overlapped(Plan& p, void* const* a) {
 
     int64_t wx, wy;
     tile_extent(p, &wx, &wy);
-    int64_t launches = 0;
     // step k over planes [*front, nf): stencil, then this step's injection
     // into, and sampling on top of, exactly those planes
     auto advance = [&](int64_t k, int* front, int nf) {
@@ -2431,16 +2433,13 @@ int64_t invoke_overlapped(Plan& p, void* const* a) {
         chunk_grid(p, wx, wy, p.resident, &zr.grid, &zr.zchunk, nf - f0);
         const StepSlots st = step_slots(p, k, p.slot);
         launch_stencil(p, st.out, st.cur, st.prev, nullptr, nullptr, &zr);
-        ++launches;
         // planes outside the stencil's range belong to the first / last range
         const int fa = f0 == zlo ? 0 : f0, fb = nf == zhi ? n0 + 1 : nf;
         if (inj.np > 0 && inj.ncells > 0 && inj_hi + 1 >= fa && inj_lo < fb) {
             launch_inject(p, inj, st.out, st.row, 0, -1, fa, fb);
-            ++launches;
         }
         if (smp.np > 0 && smp_hi + 1 >= fa && smp_lo + 1 < fb) {
             launch_sample(p, smp, st.out, st.row, std::max(fa, 1), fb);
-            ++launches;
         }
         *front = nf;
     };
@@ -2468,7 +2467,7 @@ int64_t invoke_overlapped(Plan& p, void* const* a) {
         for (int k = 0; k < K; ++k) advance(k, &front[k], zhi);  // complete the skewed steps in order
     }
     run_steps(p, K, p.nt - K2);
-    if (K2 == 0) return launches;
+    if (K2 == 0) return false;
 
     // Tail: chunk c of the three slots is final once the last step has
     // finished its planes, which needs step nt-1-i to be r * i planes further.
@@ -2491,7 +2490,7 @@ int64_t invoke_overlapped(Plan& p, void* const* a) {
         SF_CUDA(cudaEventRecord(p.ev_up[0], p.io));
         SF_CUDA(cudaStreamWaitEvent(p.stream, p.ev_up[0], 0));  // the call ends when the copies have
     }
-    return -launches;  // negative: the field is already back in host memory
+    return true;
 }
 
 void upload_any(Plan& p, void* const* a, int nargs) {
@@ -3278,7 +3277,7 @@ int sf_plan_invoke(sf_plan* p, void* const* args, int nargs) {
         if (sfb::io_overlap_eligible(*p, args, nargs)) {
             sfb::NvtxRange r("time loop with the upload / download overlapped by its first / last steps");
             try {
-                field_back = sfb::invoke_overlapped(*p, args) < 0;
+                field_back = sfb::invoke_overlapped(*p, args);
             } catch (...) {
                 // asynchronous copies may still reference the caller's buffers
                 if (p->io) cudaStreamSynchronize(p->io);
