@@ -661,10 +661,9 @@ bool pdl_enabled() {
     return on;
 }
 
-// Set while the time-skewed steps of invoke_overlapped are enqueued: there a
-// launch may follow a kernel that wrote what its producer warp reads before
-// griddepcontrol.wait (the eta flag words of a chunk), so those launches are
-// plainly stream-ordered.
+// Set for the launch that follows a chunk's eta-flag kernel in
+// invoke_overlapped: the flags are what a producer warp reads before
+// griddepcontrol.wait, so that launch is plainly stream-ordered.
 thread_local bool g_plain_launches = false;
 
 template <typename Kern>
@@ -2259,17 +2258,14 @@ double step_seconds_estimate(const Plan& p) {
 }
 
 // Chunk height: whole planes, a multiple of 32 (one eta flag word per 32
-// planes), about n0 / 16, and tall enough that one step on one chunk runs for
-// ~50 us (the skewed steps are plain launches, not graph nodes).
+// planes), about n0 / 16 and at least 64.
 int io_chunk_planes(const Plan& p) {
     const int n0 = static_cast<int>(p.n[0]);
     if (const char* e = std::getenv("SF_IO_CHUNK_PLANES")) {
         const int v = std::atoi(e);
         if (v >= 32) return v / 32 * 32;
     }
-    const double per_plane = step_seconds_estimate(p) / n0;
-    const int by_time = static_cast<int>(50e-6 / std::max(per_plane, 1e-12)) + 1;
-    return (std::max({32, n0 / 16, by_time}) + 31) / 32 * 32;
+    return (std::max(64, n0 / 16) + 31) / 32 * 32;
 }
 
 bool io_overlap_eligible(const Plan& p, void* const* a, int nargs) {
@@ -2293,10 +2289,12 @@ bool io_overlap_eligible(const Plan& p, void* const* a, int nargs) {
         }
         if (at.type != cudaMemoryTypeHost) return false;
     }
-    // worth it only where a chunk of a step is long against a launch: at least
-    // four chunks (measured: 281^3 with 32-plane chunks loses 40 %, 1024^3
-    // with 64-plane chunks gains 10 %)
-    return 4 * io_chunk_planes(p) <= p.n[0];
+    // worth it only where a chunk of a step is long against a launch (the
+    // skewed steps are stream launches, not graph nodes): at least three
+    // chunks of >= 15 us each (measured e2e: 1024^3 +11 %, 512^3 +9..19 %,
+    // 281^3 +5 %)
+    const int zc = io_chunk_planes(p);
+    return 3 * zc <= p.n[0] && step_seconds_estimate(p) * zc / static_cast<double>(p.n[0]) >= 15e-6;
 }
 
 void tile_extent(const Plan& p, int64_t* wx, int64_t* wy) {
@@ -2375,8 +2373,10 @@ bool invoke_overlapped(Plan& p, void* const* a) {
     // steps worth of compute that fit under the upload / the copy back
     const double t_step = step_seconds_estimate(p);
     const double field_bytes = 4.0 * static_cast<double>(p.n[0]) * p.n[1] * p.n[2];
-    const int k_up = static_cast<int>(5.0 * field_bytes / 55e9 / t_step) + 1;
-    const int k_down = static_cast<int>(1.2 * 3.0 * field_bytes / 55e9 / t_step) + 1;
+    // (a skewed step costs ~12 us of launch gaps and ramp per chunk on top of its work)
+    const double t_chunk = t_step * zc / n0, eff = t_chunk / (t_chunk + 12e-6);
+    const int k_up = static_cast<int>(eff * 5.0 * field_bytes / 55e9 / t_step) + 1;
+    const int k_down = static_cast<int>(eff * 1.2 * 3.0 * field_bytes / 55e9 / t_step) + 1;
     int K = static_cast<int>(std::min<int64_t>(p.nt, std::min(k_up, 128)));
     if (const char* e = std::getenv("SF_IO_STEPS")) {
         const int v = std::atoi(e);
@@ -2443,12 +2443,11 @@ bool invoke_overlapped(Plan& p, void* const* a) {
         }
         *front = nf;
     };
-    struct PlainLaunches {  // see g_plain_launches
-        PlainLaunches() { g_plain_launches = true; }
-        ~PlainLaunches() { g_plain_launches = false; }
+    struct PlainLaunch {  // see g_plain_launches
+        PlainLaunch() { g_plain_launches = true; }
+        ~PlainLaunch() { g_plain_launches = false; }
     };
     {
-        PlainLaunches plain;
         std::vector<int> front(static_cast<size_t>(K), zlo);
         for (int c = 0; c < nchunks; ++c) {
             const int up = std::min(n0, (c + 1) * zc);  // planes [0, up) have arrived
@@ -2461,7 +2460,15 @@ bool invoke_overlapped(Plan& p, void* const* a) {
                 const int avail = k == 0 ? up : front[k - 1] < zhi ? front[k - 1] : up == n0 ? n0 : zhi;
                 const int nf = std::min(zhi, avail - r);
                 if (nf <= front[k]) break;  // later steps trail this one
-                advance(k, &front[k], nf);
+                if (k == 0) {
+                    // right behind the flags kernel: a plain launch, so the
+                    // producer warp's early flag reads are ordered after it;
+                    // the launches that follow may overlap their predecessor
+                    PlainLaunch plain;
+                    advance(k, &front[k], nf);
+                } else {
+                    advance(k, &front[k], nf);
+                }
             }
         }
         for (int k = 0; k < K; ++k) advance(k, &front[k], zhi);  // complete the skewed steps in order
@@ -2474,7 +2481,6 @@ bool invoke_overlapped(Plan& p, void* const* a) {
     // Each pass advances all K2 steps just that far, then the chunk's copy
     // back starts on the copy stream while the next pass runs.
     {
-        PlainLaunches plain;
         std::vector<int> front(static_cast<size_t>(K2), zlo);
         float* host_u = static_cast<float*>(a[0]);
         for (int c = 0; c < nchunks; ++c) {
