@@ -168,7 +168,11 @@ struct sf_plan {
     int vec_rpl = 1;  // vector kernel: rows of four points per lane (1 or 2)
     bool vec_aq = true;  // 16-warp radius-4 ring kernel with the a0 register queue (SF_VEC_AQ=0: ring loads)
     // kernel selector: kRplAq picks the a0-queue instance (geometry as rpl = 1)
-    int vec_kernel_rpl() const { return vec_aq && vec_warps == 16 && vec_rpl == 1 ? kRplAq : vec_rpl; }
+    int vec_kernel_rpl() const {
+        const bool shape_ok = vec_rpl == 1 && tile_nx == 2 && ac.radius == 4;
+        return shape_ok && ((vec_aq && vec_warps == 16) || (vec_aq8 && vec_warps == 8)) ? kRplAq : vec_rpl;
+    }
+    bool vec_aq8 = false;  // the same for the 8-warp 64 x 16 tiles (SF_VEC_AQ8=1; A/B)
     int tma_stages = 4;
     int stages_override = 0;  // autotune: > 0 forces the pipeline depth
     size_t tma_smem = 0;
@@ -535,10 +539,14 @@ const void* vec_ptr_r(int warps, int nx, int rpl) {
         return warps == 4   ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4, false, 8>)
                : warps == 8 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 8, false, 8>)
                             : nullptr;
-    if (warps == 16 && rpl == kRplAq)  // the same with the a0 register queue (SF_VEC_AQ=1)
-        return RR == 4 ? reinterpret_cast<const void*>(
-                             &acoustic3d_vec_kernel<4, FWD, 16, false, 16, 1, true>)
-                       : nullptr;
+    if (rpl == kRplAq) {  // radius 4, 64-wide tiles, a0 register queue
+        if (RR != 4) return nullptr;
+        return warps == 16 ? reinterpret_cast<const void*>(
+                                 &acoustic3d_vec_kernel<4, FWD, 16, false, 16, 1, true>)
+               : warps == 8 ? reinterpret_cast<const void*>(
+                                  &acoustic3d_vec_kernel<4, FWD, 8, false, 16, 1, true>)
+                            : nullptr;
+    }
     if (warps == 16)  // 64 x 32 tiles, one CTA per SM (radius 4 only)
         return RR == 4 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<4, FWD, 16>) : nullptr;
     return warps == 4 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4>)
@@ -687,8 +695,10 @@ void launch_vec(int r, int warps, int nx, int rpl, dim3 g, size_t smem, cudaStre
     const dim3 b(32 * (warps + 1));  // + the TMA producer warp
 #define SF_V(RR)                                                                             \
     case RR:                                                                                 \
-        if (rpl == kRplAq)                                                                   \
+        if (rpl == kRplAq && warps == 16)                                                    \
             launch_pdl(acoustic3d_vec_kernel<4, FWD, 16, false, 16, 1, true>, g, b, smem, st, A); \
+        else if (rpl == kRplAq)                                                              \
+            launch_pdl(acoustic3d_vec_kernel<4, FWD, 8, false, 16, 1, true>, g, b, smem, st, A); \
         else if (rpl == 2 && nx == 1)                                                        \
             launch_pdl(acoustic3d_vec_kernel<RR, FWD, 2, false, 8, 2>, g, b, smem, st, A);   \
         else if (rpl == 2)                                                                   \
@@ -2048,6 +2058,7 @@ void enable_tma(Plan& p) {
         // cover the interior with fewer padded points (FWI: 64 wide, one set
         // of maps serves the forward and gradient kernels)
         p.tile_nx = 2;
+        if (const char* e = std::getenv("SF_VEC_AQ8")) p.vec_aq8 = std::atoi(e) != 0;
         if (p.kind != Plan::FWI) {
             const int r = p.ac.radius;
             auto cover = [&](int nx, int warps) {
