@@ -92,14 +92,10 @@ def pinned_array(shape, dtype=np.float32, like=None):
     import torch
     tdt = {np.float32: torch.float32, np.int32: torch.int32}[np.dtype(dtype).type]
     t = torch.zeros(tuple(shape), dtype=tdt, pin_memory=True)
-    a = t.numpy()
-    _PINNED_KEEPALIVE[id(a)] = t
+    a = t.numpy()  # shares (and keeps alive) the tensor's page-locked storage
     if like is not None:
         a[...] = like
     return a
-
-
-_PINNED_KEEPALIVE = {}
 
 
 class GridFunction:
