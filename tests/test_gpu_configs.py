@@ -293,10 +293,20 @@ def test_c3o8_full_time_loop_vs_reference(sf, ref):
 
 def test_c4_full_time_loop_vs_reference(sf, ref):
     """All 1000 steps take the 16-thread host reference ~15 min, so the
-    default GPU run stops at 200 steps (~3 min); SF_LONG_TESTS=1 runs the full
-    loop (profiles/r2_full_time_loop_parity.log: bitwise after 1000 steps)."""
+    default GPU run stops at 60 steps (~1.5 min) with the overlapped invoke
+    set to 30 skewed head steps, 10 graph steps and 20 skewed tail steps;
+    SF_LONG_TESTS=1 runs the full loop with the default split
+    (profiles/r2_full_time_loop_parity_final.log: bitwise after 1000 steps on
+    the final kernels)."""
     import os
-    _full_loop_vs_reference(sf, ref, "c4", None if os.environ.get("SF_LONG_TESTS") == "1" else 200)
+    if os.environ.get("SF_LONG_TESTS") == "1":
+        _full_loop_vs_reference(sf, ref, "c4")
+        return
+    os.environ["SF_IO_STEPS"], os.environ["SF_IO_TAIL_STEPS"] = "30", "20"
+    try:
+        _full_loop_vs_reference(sf, ref, "c4", 60)
+    finally:
+        del os.environ["SF_IO_STEPS"], os.environ["SF_IO_TAIL_STEPS"]
 
 
 def test_c5_full_algorithm_reduced_nt_vs_port(sf, port):
