@@ -124,6 +124,7 @@ struct PointSet {
 // rows-per-lane selector of the 16-warp radius-4 ring kernel with the a0
 // register queue (one row per lane)
 constexpr int kRplAq = 17;
+constexpr int kRplAq2 = 18;  // the same, two planes per pass (SF_VEC_AQ2=1; A/B)
 
 struct sf_plan {
     enum Kind { ACOUSTIC, DIFFUSION, FWI } kind;
@@ -170,8 +171,10 @@ struct sf_plan {
     // kernel selector: kRplAq picks the a0-queue instance (geometry as rpl = 1)
     int vec_kernel_rpl() const {
         const bool shape_ok = vec_rpl == 1 && tile_nx == 2 && ac.radius == 4;
+        if (shape_ok && vec_aq && vec_aq2 && vec_warps == 16) return kRplAq2;
         return shape_ok && ((vec_aq && vec_warps == 16) || (vec_aq8 && vec_warps == 8)) ? kRplAq : vec_rpl;
     }
+    bool vec_aq2 = false;
     bool vec_aq8 = false;  // the same for the 8-warp 64 x 16 tiles (SF_VEC_AQ8=1; A/B)
     int tma_stages = 4;
     int stages_override = 0;  // autotune: > 0 forces the pipeline depth
@@ -539,6 +542,10 @@ const void* vec_ptr_r(int warps, int nx, int rpl) {
         return warps == 4   ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 4, false, 8>)
                : warps == 8 ? reinterpret_cast<const void*>(&acoustic3d_vec_kernel<RR, FWD, 8, false, 8>)
                             : nullptr;
+    if (rpl == kRplAq2)
+        return RR == 4 && warps == 16 ? reinterpret_cast<const void*>(
+                                            &acoustic3d_vec_kernel<4, FWD, 16, false, 16, 1, true, 2>)
+                                      : nullptr;
     if (rpl == kRplAq) {  // radius 4, 64-wide tiles, a0 register queue
         if (RR != 4) return nullptr;
         return warps == 16 ? reinterpret_cast<const void*>(
@@ -695,7 +702,9 @@ void launch_vec(int r, int warps, int nx, int rpl, dim3 g, size_t smem, cudaStre
     const dim3 b(32 * (warps + 1));  // + the TMA producer warp
 #define SF_V(RR)                                                                             \
     case RR:                                                                                 \
-        if (rpl == kRplAq && warps == 16)                                                    \
+        if (rpl == kRplAq2)                                                                  \
+            launch_pdl(acoustic3d_vec_kernel<4, FWD, 16, false, 16, 1, true, 2>, g, b, smem, st, A); \
+        else if (rpl == kRplAq && warps == 16)                                               \
             launch_pdl(acoustic3d_vec_kernel<4, FWD, 16, false, 16, 1, true>, g, b, smem, st, A); \
         else if (rpl == kRplAq)                                                              \
             launch_pdl(acoustic3d_vec_kernel<4, FWD, 8, false, 16, 1, true>, g, b, smem, st, A); \
@@ -2077,6 +2086,7 @@ void enable_tma(Plan& p) {
                 }
             }
             if (const char* e = std::getenv("SF_VEC_AQ")) p.vec_aq = std::atoi(e) != 0;
+            if (const char* e = std::getenv("SF_VEC_AQ2")) p.vec_aq2 = std::atoi(e) != 0;
             // two rows per lane: same tile, half the consumer warps
             p.vec_rpl = 1;
             if (const char* e = std::getenv("SF_VEC_RPL"))

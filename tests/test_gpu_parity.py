@@ -343,7 +343,8 @@ VARIANTS = [{}, {"SF_VEC": "0"}, {"SF_NO_TMA": "1"}, {"SF_VEC": "0", "SF_TMA": "
             {"SF_VECQ2": "1", "SF_TMA_STAGES": "3"}, {"SF_VECQ_FORM": "free"},
             {"SF_VECQ_FORM": "pinned"}, {"SF_VECQ_FORM": "tmem"}, {"SF_VEC_WARPS": "16"},
             {"SF_VEC_NX": "1", "SF_VEC_WARPS": "8"}, {"SF_VEC_WARPS": "16", "SF_VEC_AQ": "1"}, {"SF_VEC_WARPS": "16", "SF_VEC_AQ": "0"},
-            {"SF_VEC_WARPS": "8", "SF_VEC_AQ8": "1"},
+            {"SF_VEC_WARPS": "8", "SF_VEC_AQ8": "1"}, {"SF_VEC_WARPS": "16", "SF_VEC_AQ2": "1"},
+            {"SF_VEC_WARPS": "16", "SF_VEC_AQ2": "1", "SF_ZCHUNKS": "3"},
             {"SF_VECQ_FORM": "last"}, {"SF_VEC_WARPS": "8", "SF_VECQ_FORM": "last"},
             {"SF_VEC_WARPS": "12"}, {"SF_VEC_WARPS": "12", "SF_VECQ_FORM": "last"}]
 
